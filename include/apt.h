@@ -1,0 +1,175 @@
+/* apt.h — C ABI of the B200-native APT arbitrary-precision W_p x A_q integer MatMul.
+ *
+ * The operation (arXiv 2508.19087, PAPER.md = "P:<line>"):
+ *   signed n-bit integer codes are converted losslessly to bipolar-INT by flipping
+ *   the sign bit (§3.1: x' = 2x + 1), decomposed into n bit-planes and
+ *   packed into 32-bit words concatenated into one "unified matrix" (§4.1);
+ *   the GEMM multiplies the planes and reassembles the exact result by shift-add
+ *   (§3.2: Y = sum_{i,j} 2^(i+j) Y^(i,j)), with the reassembly kept on chip
+ *   (§4.2).  An optional epilogue scales the exact int32 result by
+ *   per-channel / per-token fp32 scales (linear quantization W = s*W_hat)
+ *   and rounds once to fp16.
+ *
+ * Orientation (reading Q2): A = activations [M, K] (abits = p_a bits),
+ * W = weights [N, K] (wbits = p_w bits), both K-contiguous;
+ *     Y[m][n] = sum_{k<K} A[m][k] * W[n][k]             (signed codes, exact)
+ *     Y'[m][n] = sum_{k<K} (2A+1)[m][k] * (2W+1)[n][k]  (bipolar product)
+ *
+ * General contract
+ *   - Every pointer is a DEVICE pointer unless marked "host".
+ *   - All calls taking a stream are stream-ordered and asynchronous; the library never
+ *     synchronizes, never allocates device memory, and keeps no per-call state.
+ *     Argument errors are returned synchronously before anything is launched.
+ *   - The caller owns every buffer (in practice torch tensors).
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - Thread-safe: the only global state is a mutex-guarded cache of device attributes.
+ *   - There is no CPU fallback: with no CUDA device every launching call returns APT_ERR_CUDA.
+ */
+#ifndef APT_H_
+#define APT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define APT_API __attribute__((visibility("default")))
+#else
+#define APT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APT_ABI_VERSION 1
+#define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
+
+typedef enum {
+  APT_OK = 0,
+  APT_ERR_INVALID_ARGUMENT = 1, /* null pointer, bits outside [1,8], dim <= 0, ld < K, misalignment,
+                                   shape mismatch between the packed operands and M/N/K           */
+  APT_ERR_UNSUPPORTED = 2,      /* int32 overflow bound exceeded (reading Q8) or a config that is
+                                   illegal for the shape                                            */
+  APT_ERR_WORKSPACE = 3,        /* workspace missing or smaller than apt_gemm_workspace_bytes()      */
+  APT_ERR_CUDA = 4              /* a CUDA launch/runtime error (cudaGetLastError) or no device        */
+} apt_status;
+
+typedef enum {
+  APT_ENC_SIGNED = 0, /* codes are signed n-bit integers x in [-2^(n-1), 2^(n-1)-1]; n = 1 -> {-1, 0}
+                         (reading Q4)                                                 */
+  APT_ENC_BIPOLAR = 1 /* codes are bipolar values x' (odd, |x'| <= 2^n - 1); converted by
+                         x = (x' - 1) / 2.  int8 storage limits this encoding to n <= 7.     */
+} apt_encoding;
+
+/* The packed "unified matrix" (SPEC PackedPlanes S:35-41, with 32-bit words per P:252).
+ *   planes  : uint32 [bits][rows][k_words], plane-major, one contiguous buffer.
+ *             Plane i holds bit i of the bipolar pattern u = x + 2^(n-1) (the sign-bit-flipped
+ *             two's-complement code).  Element c of a row is bit (c % 32) of word (c / 32),
+ *             LSB first (reading Q5).  Pad elements c in [k, Kpad) hold the signed code 0,
+ *             i.e. u = 2^(n-1) (reading Q6), so they contribute exactly 0 to signed products.
+ *             Must be 16-byte aligned.
+ *   row_sum : int32 [rows], sum_{c<k} of the signed codes of the row (used by the rank-1 terms of
+ *             the epilogue; SURVEY §8c identities I2/I3).
+ *   rows, k : logical shape; k_words = Kpad / 32; bits = n in [1, 8].                              */
+typedef struct {
+  int32_t rows;
+  int32_t k;
+  int32_t k_words;
+  int32_t bits;
+  uint32_t* planes;
+  int32_t* row_sum;
+} apt_packed;
+
+/* Host.  Bytes of the `planes` buffer for a rows x k matrix of n-bit codes:
+ * bits * rows * round_up(k,256)/32 * 4.  Returns 0 for invalid arguments. */
+APT_API size_t apt_packed_plane_bytes(int32_t rows, int32_t k, int32_t bits);
+
+/* Decomposition & reassembly (§4.1 Steps 1-3) on the device.
+ *   codes       : int8 [rows][ld] row-major, element (r, c) at codes[r*ld + c], c < k.
+ *   out         : host struct; out->planes (apt_packed_plane_bytes) and out->row_sum (rows int32)
+ *                 must point to caller-allocated device buffers.  The call fills rows/k/k_words/bits
+ *                 and writes both buffers (every word, including the padding).
+ *   range_error : nullable device int32.  If some code is outside the declared range, the kernel
+ *                 stores 1 + (linear index r*k + c of one such code) there (first writer wins; the
+ *                 caller zeroes it beforehand and reads it after its own synchronization).
+ *                 Out-of-range codes are packed as u = (x + 2^(n-1)) mod 2^n.
+ * Errors: APT_ERR_INVALID_ARGUMENT (null codes/out/buffers, rows <= 0, k <= 0, ld < k,
+ *         bits outside [1,8], bipolar with bits > 7, misaligned planes), APT_ERR_CUDA. */
+APT_API apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k, int64_t ld, int32_t bits,
+                            apt_encoding enc, apt_packed* out, int32_t* range_error, void* stream);
+
+/* Per-channel / per-token fp32 scales for APT_OUT_F16_SCALED (reading Q10):
+ *   out[m][n] = RN_fp16( ((float)Y[m][n] * w_scale[n]) * a_scale[m] ), fp32 arithmetic,
+ *   one final round-to-nearest-even to fp16 (overflow -> +-inf). */
+typedef struct {
+  const float* w_scale; /* [N], required for APT_OUT_F16_SCALED */
+  const float* a_scale; /* [M] per token, or NULL (== 1)        */
+} apt_scales;
+
+typedef enum {
+  APT_OUT_I32_SIGNED = 0,  /* int32 Y  = A . W^T over signed codes (reading Q1, default)        */
+  APT_OUT_I32_BIPOLAR = 1, /* int32 Y' = A' . W'^T over bipolar values (Fig. 4)          */
+  APT_OUT_F16_SCALED = 2   /* fp16 scaled Y (needs scales->w_scale)                             */
+} apt_out_kind;
+
+typedef enum {
+  APT_LAYOUT_ROW = 0, /* out[m * ldo + n], ldo >= N                                       */
+  APT_LAYOUT_COL = 1  /* out[n * ldo + m] = Y^T, ldo >= M (contiguous N-slices for the TP gather) */
+} apt_layout;
+
+typedef enum {
+  APT_KERNEL_AUTO = 0,
+  APT_KERNEL_MMA_SPLITK = 1, /* register-rebuild mma.sync u8 kernel, split-K reduced in a thread-block
+                                cluster through distributed shared memory (decode / small M)     */
+  APT_KERNEL_TC = 2          /* tcgen05 kind::i8 kernel: weights rebuilt in registers -> TMEM (A operand),
+                                tokens via TMA from the int8 token workspace, s32 accumulator in TMEM */
+} apt_kernel;
+
+/* Kernel configuration (the B200 analogue of the paper's tunable hyperparameters, §5.1).
+ *   kernel   : apt_kernel
+ *   w_digit, a_digit : digit widths of the operand rebuild; this build uses full width (= bits),
+ *                      one MMA pass for every p, q <= 8
+ *   bm       : weight rows per CTA tile (MMA M side)
+ *   bn       : tokens per CTA tile (MMA N side)
+ *   bk       : K elements per pipeline step
+ *   stages   : pipeline depth (TC kernel)
+ *   split_k  : K splits (MMA_SPLITK kernel: the cluster size, 1..8)
+ *   cta_pair : 1 = cta_group::2 pairs (TC kernel), 0 = single CTA                                   */
+typedef struct {
+  int32_t kernel, w_digit, a_digit, bm, bn, bk, stages, split_k, cta_pair;
+} apt_config;
+
+/* Host, pure and deterministic (replaces the paper's lookup table + search, §5.2).
+ * p = wbits, q = abits as in the north_star's "W_p x A_q".
+ * Errors: APT_ERR_INVALID_ARGUMENT (dims <= 0, bits outside [1,8], null out),
+ *         APT_ERR_UNSUPPORTED (int32 bound, reading Q8). */
+APT_API apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits,
+                             apt_config* out /* host */);
+
+/* Host.  Device workspace bytes apt_gemm needs for (cfg, M, N, K).  0 = none. */
+APT_API size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K);
+
+/* The W_p x A_q GEMM (§3.2 + §4.2): out = epilogue(A . W^T), exact in int32.
+ *   W, A      : host structs describing device buffers produced by apt_pack_bipolar
+ *               (W->rows == N, A->rows == M, W->k == A->k == K, W->bits == wbits, A->bits == abits).
+ *   scales    : host struct (nullable unless kind == APT_OUT_F16_SCALED).
+ *   out       : int32 (I32 kinds) or fp16 (F16 kind) buffer in `layout` with leading dimension ldo.
+ *   cfg       : host, NULL -> apt_select_config.
+ *   workspace : device scratch of apt_gemm_workspace_bytes(cfg, M, N, K) bytes (nullable if 0).
+ * Bound (reading Q8): requires Kpad * (2^abits - 1) * (2^wbits - 1) < 2^31, else APT_ERR_UNSUPPORTED.
+ * Errors: APT_ERR_INVALID_ARGUMENT, APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ERR_CUDA. */
+APT_API apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, const apt_packed* W,
+                    const apt_packed* A, const apt_scales* scales, apt_out_kind kind, apt_layout layout,
+                    void* out, int64_t ldo, const apt_config* cfg, void* workspace, size_t ws_bytes,
+                    void* stream);
+
+/* Host.  Human-readable name of a status code (static storage). */
+APT_API const char* apt_status_string(apt_status s);
+
+/* Host.  ABI version (APT_ABI_VERSION) of the loaded library. */
+APT_API int32_t apt_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APT_H_ */

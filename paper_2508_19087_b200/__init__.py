@@ -1,0 +1,12 @@
+"""B200-native APT-LLM arbitrary-precision W_p x A_q integer MatMul (arXiv 2508.19087).
+
+Public API (torch tensors in, CUDA kernels of libapt.so underneath):
+    pack(codes, bits)                    -> Packed bit-planes          (apt_pack_bipolar)
+    gemm(W, A, out_kind=..., ...)         -> int32 / fp16 result        (apt_gemm)
+    select_config(M, N, K, wbits, abits) -> kernel configuration       (apt_select_config)
+    tp.TPLinear / tp.tp_gemm             -> N-split tensor parallel GEMM + all-gather
+"""
+from .api import Packed, alloc_packed, gemm, kpad, pack, select_config, workspace_bytes  # noqa: F401
+from . import _lib  # noqa: F401
+
+__all__ = ["Packed", "alloc_packed", "gemm", "kpad", "pack", "select_config", "workspace_bytes"]

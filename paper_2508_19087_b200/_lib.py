@@ -1,0 +1,84 @@
+"""ctypes binding of libapt.so (include/apt.h).  Argument marshalling only.
+
+The library is built in-tree by ``__graft_entry__.build()``; importing this module without it raises
+immediately — there is no fallback implementation of any kind.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libapt.so")
+
+APT_OK, APT_ERR_INVALID_ARGUMENT, APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ERR_CUDA = range(5)
+APT_ENC_SIGNED, APT_ENC_BIPOLAR = 0, 1
+APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
+APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
+APT_KERNEL_AUTO, APT_KERNEL_MMA_SPLITK, APT_KERNEL_TC = 0, 1, 2
+
+EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_select_config", "apt_gemm_workspace_bytes",
+            "apt_gemm", "apt_status_string", "apt_abi_version"]
+
+
+class AptPacked(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int32), ("k", ctypes.c_int32), ("k_words", ctypes.c_int32),
+                ("bits", ctypes.c_int32), ("planes", ctypes.c_void_p), ("row_sum", ctypes.c_void_p)]
+
+
+class AptScales(ctypes.Structure):
+    _fields_ = [("w_scale", ctypes.c_void_p), ("a_scale", ctypes.c_void_p)]
+
+
+class AptConfig(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("kernel", "w_digit", "a_digit", "bm", "bn", "bk", "stages", "split_k", "cta_pair")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class AptError(RuntimeError):
+    def __init__(self, fn, status):
+        self.status = status
+        super().__init__(f"{fn} failed: {status_string(status)} ({status})")
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no fallback path exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.apt_packed_plane_bytes.restype = ctypes.c_size_t
+        L.apt_packed_plane_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+        L.apt_pack_bipolar.restype = ctypes.c_int
+        L.apt_pack_bipolar.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                       ctypes.c_int32, ctypes.c_int, ctypes.POINTER(AptPacked), ctypes.c_void_p,
+                                       ctypes.c_void_p]
+        L.apt_select_config.restype = ctypes.c_int
+        L.apt_select_config.argtypes = [ctypes.c_int32] * 5 + [ctypes.POINTER(AptConfig)]
+        L.apt_gemm_workspace_bytes.restype = ctypes.c_size_t
+        L.apt_gemm_workspace_bytes.argtypes = [ctypes.POINTER(AptConfig), ctypes.c_int32, ctypes.c_int32,
+                                               ctypes.c_int32]
+        L.apt_gemm.restype = ctypes.c_int
+        L.apt_gemm.argtypes = [ctypes.c_int32] * 5 + [ctypes.POINTER(AptPacked), ctypes.POINTER(AptPacked),
+                                                      ctypes.POINTER(AptScales), ctypes.c_int, ctypes.c_int,
+                                                      ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(AptConfig),
+                                                      ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+        L.apt_status_string.restype = ctypes.c_char_p
+        L.apt_status_string.argtypes = [ctypes.c_int]
+        L.apt_abi_version.restype = ctypes.c_int32
+        L.apt_abi_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def status_string(status: int) -> str:
+    return lib().apt_status_string(status).decode()
+
+
+def check(fn: str, status: int):
+    if status != APT_OK:
+        raise AptError(fn, status)

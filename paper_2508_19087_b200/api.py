@@ -1,0 +1,151 @@
+"""Thin torch-facing binding over the C ABI (argument marshalling only).
+
+Every step of the hot path runs in libapt.so's CUDA kernels; torch provides device memory,
+streams and process groups.  Names follow include/apt.h and the paper's notation:
+``W`` = weights [N, K] (``wbits`` = p_w), ``A`` = activations [M, K] (``abits`` = p_a).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+KPAD_QUANTUM = 256
+
+_OUT_KINDS = {"i32": L.APT_OUT_I32_SIGNED, "bipolar": L.APT_OUT_I32_BIPOLAR, "f16": L.APT_OUT_F16_SCALED}
+_LAYOUTS = {"row": L.APT_LAYOUT_ROW, "col": L.APT_LAYOUT_COL}
+_ENCODINGS = {"signed": L.APT_ENC_SIGNED, "bipolar": L.APT_ENC_BIPOLAR}
+
+
+def kpad(k: int) -> int:
+    return -(-k // KPAD_QUANTUM) * KPAD_QUANTUM
+
+
+def _stream_handle(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def _require_cuda(t: torch.Tensor, name: str):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the APT path has no CPU implementation)")
+
+
+@dataclass
+class Packed:
+    """The packed "unified matrix": planes [bits][rows][k_words] uint32 (stored as int32
+    tensor), row_sum [rows] int32."""
+    planes: torch.Tensor
+    row_sum: torch.Tensor
+    rows: int
+    k: int
+    bits: int
+
+    @property
+    def k_words(self) -> int:
+        return kpad(self.k) // 32
+
+    def struct(self) -> L.AptPacked:
+        return L.AptPacked(self.rows, self.k, self.k_words, self.bits, self.planes.data_ptr(),
+                           self.row_sum.data_ptr())
+
+    def narrow_rows(self, start: int, length: int) -> "Packed":
+        """Rows [start, start+length) as a new packed matrix (copies the plane slices)."""
+        planes = self.planes[:, start:start + length].contiguous()
+        return Packed(planes, self.row_sum[start:start + length].contiguous(), length, self.k, self.bits)
+
+
+def alloc_packed(rows: int, k: int, bits: int, device) -> Packed:
+    kw = kpad(k) // 32
+    planes = torch.empty((bits, rows, kw), dtype=torch.int32, device=device)
+    row_sum = torch.empty((rows,), dtype=torch.int32, device=device)
+    return Packed(planes, row_sum, rows, k, bits)
+
+
+def pack(codes: torch.Tensor, bits: int, encoding: str = "signed", out: Packed | None = None,
+         range_error: torch.Tensor | None = None, stream=None) -> Packed:
+    """apt_pack_bipolar: int8 codes [rows, k] (row stride ``codes.stride(0)``) -> Packed."""
+    _require_cuda(codes, "codes")
+    if codes.dtype != torch.int8 or codes.dim() != 2 or codes.stride(1) != 1:
+        raise ValueError("codes must be a 2-D int8 tensor with unit stride along K")
+    rows, k = codes.shape
+    if out is None:
+        out = alloc_packed(rows, k, bits, codes.device)
+    st = out.struct()
+    rc = L.lib().apt_pack_bipolar(codes.data_ptr(), rows, k, codes.stride(0), bits, _ENCODINGS[encoding],
+                                  ctypes.byref(st), range_error.data_ptr() if range_error is not None else None,
+                                  _stream_handle(stream))
+    L.check("apt_pack_bipolar", rc)
+    return out
+
+
+def select_config(M: int, N: int, K: int, wbits: int, abits: int) -> dict:
+    """apt_select_config (p = wbits, q = abits)."""
+    c = L.AptConfig()
+    L.check("apt_select_config", L.lib().apt_select_config(M, N, K, wbits, abits, ctypes.byref(c)))
+    return c.as_dict()
+
+
+def _config_struct(cfg: dict | None):
+    if cfg is None:
+        return None
+    c = L.AptConfig()
+    for n, _ in c._fields_:
+        setattr(c, n, int(cfg[n]))
+    return c
+
+
+def workspace_bytes(cfg: dict, M: int, N: int, K: int) -> int:
+    c = _config_struct(cfg)
+    return int(L.lib().apt_gemm_workspace_bytes(ctypes.byref(c), M, N, K))
+
+
+def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_scale: torch.Tensor | None = None,
+         a_scale: torch.Tensor | None = None, out: torch.Tensor | None = None, config: dict | None = None,
+         workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """apt_gemm: Y = A . W^T (exact int32), Y' (bipolar), or fp16-scaled, in row ([M,N]) or col
+    ([N,M]) layout."""
+    M, N, K = A.rows, W.rows, W.k
+    if A.k != K:
+        raise ValueError("A and W have different K")
+    _require_cuda(W.planes, "W.planes")
+    _require_cuda(A.planes, "A.planes")
+    kind = _OUT_KINDS[out_kind]
+    lay = _LAYOUTS[layout]
+    shape = (M, N) if lay == L.APT_LAYOUT_ROW else (N, M)
+    dtype = torch.float16 if kind == L.APT_OUT_F16_SCALED else torch.int32
+    if out is None:
+        out = torch.empty(shape, dtype=dtype, device=W.planes.device)
+    if out.dtype != dtype or out.dim() != 2 or out.stride(1) != 1 or tuple(out.shape) != shape:
+        raise ValueError(f"out must be a {dtype} tensor of shape {shape} with unit inner stride")
+    sc = None
+    if w_scale is not None or a_scale is not None:
+        for t, nm in ((w_scale, "w_scale"), (a_scale, "a_scale")):
+            if t is not None:
+                _require_cuda(t, nm)
+                if t.dtype != torch.float32 or not t.is_contiguous():
+                    raise ValueError(f"{nm} must be contiguous fp32")
+        sc = L.AptScales(w_scale.data_ptr() if w_scale is not None else None,
+                         a_scale.data_ptr() if a_scale is not None else None)
+    c = _config_struct(config)
+    if c is None:
+        ws_need = 0
+    else:
+        ws_need = int(L.lib().apt_gemm_workspace_bytes(ctypes.byref(c), M, N, K))
+    if config is None:
+        sel = L.AptConfig()
+        L.check("apt_select_config", L.lib().apt_select_config(M, N, K, W.bits, A.bits, ctypes.byref(sel)))
+        ws_need = int(L.lib().apt_gemm_workspace_bytes(ctypes.byref(sel), M, N, K))
+    if ws_need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < ws_need):
+        workspace = torch.empty((ws_need,), dtype=torch.uint8, device=W.planes.device)
+    ws_ptr = workspace.data_ptr() if workspace is not None else None
+    ws_len = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    ws, as_ = W.struct(), A.struct()
+    rc = L.lib().apt_gemm(M, N, K, W.bits, A.bits, ctypes.byref(ws), ctypes.byref(as_),
+                          ctypes.byref(sc) if sc is not None else None, kind, lay, out.data_ptr(), out.stride(0),
+                          ctypes.byref(c) if c is not None else None, ws_ptr, ws_len, _stream_handle(stream))
+    L.check("apt_gemm", rc)
+    return out

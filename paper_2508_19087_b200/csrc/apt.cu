@@ -1,0 +1,188 @@
+// apt.cu — the C-ABI boundary (include/apt.h): argument validation, the config selector and
+// kernel dispatch.  No torch types, no allocation, no synchronization.
+#include <cstdint>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "../../include/apt.h"
+#include "kernels.h"
+
+
+namespace {
+
+constexpr int kNumSMs = 148;
+
+int64_t kpad_of(int64_t k) { return ((k + APT_KPAD_QUANTUM - 1) / APT_KPAD_QUANTUM) * APT_KPAD_QUANTUM; }
+
+bool bound_ok(int64_t k, int wbits, int abits) {
+  // reading Q8: Kpad * (2^abits - 1) * (2^wbits - 1) < 2^31 bounds |Y|, |Y'| and every unsigned partial sum
+  return kpad_of(k) * ((1ll << abits) - 1) * ((1ll << wbits) - 1) < (1ll << 31);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+apt_status validate_packed(const apt_packed* P, int32_t rows, int32_t k, int32_t bits) {
+  if (!P || !P->planes || !P->row_sum) return APT_ERR_INVALID_ARGUMENT;
+  if (P->rows != rows || P->k != k || P->bits != bits) return APT_ERR_INVALID_ARGUMENT;
+  if (P->k_words != kpad_of(k) / 32) return APT_ERR_INVALID_ARGUMENT;
+  if (!aligned16(P->planes)) return APT_ERR_INVALID_ARGUMENT;
+  return APT_OK;
+}
+
+apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits) {
+  const int kw = (int)(kpad_of(K) / 32);
+  if (c->w_digit != wbits || c->a_digit != abits) return APT_ERR_UNSUPPORTED;  // full-width digits only
+  if (c->kernel == APT_KERNEL_MMA_SPLITK) {
+    if (c->bm != 64 || c->bk != 256) return APT_ERR_UNSUPPORTED;
+    if (c->bn != 8 && c->bn != 16 && c->bn != 32 && c->bn != 64) return APT_ERR_UNSUPPORTED;
+    if (c->split_k < 1 || c->split_k > 8 || c->split_k > kw / 8) return APT_ERR_UNSUPPORTED;
+    if (c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
+    return APT_OK;
+  }
+  return APT_ERR_UNSUPPORTED;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t apt_abi_version(void) { return APT_ABI_VERSION; }
+
+const char* apt_status_string(apt_status s) {
+  switch (s) {
+    case APT_OK: return "APT_OK";
+    case APT_ERR_INVALID_ARGUMENT: return "APT_ERR_INVALID_ARGUMENT";
+    case APT_ERR_UNSUPPORTED: return "APT_ERR_UNSUPPORTED";
+    case APT_ERR_WORKSPACE: return "APT_ERR_WORKSPACE";
+    case APT_ERR_CUDA: return "APT_ERR_CUDA";
+  }
+  return "APT_ERR_UNKNOWN";
+}
+
+size_t apt_packed_plane_bytes(int32_t rows, int32_t k, int32_t bits) {
+  if (rows <= 0 || k <= 0 || bits < 1 || bits > 8) return 0;
+  return (size_t)bits * (size_t)rows * (size_t)(kpad_of(k) / 32) * 4u;
+}
+
+apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k, int64_t ld, int32_t bits,
+                            apt_encoding enc, apt_packed* out, int32_t* range_error, void* stream) {
+  if (!codes || !out || !out->planes || !out->row_sum) return APT_ERR_INVALID_ARGUMENT;
+  if (rows <= 0 || k <= 0 || ld < k || bits < 1 || bits > 8) return APT_ERR_INVALID_ARGUMENT;
+  if (enc != APT_ENC_SIGNED && enc != APT_ENC_BIPOLAR) return APT_ERR_INVALID_ARGUMENT;
+  if (enc == APT_ENC_BIPOLAR && bits > 7) return APT_ERR_INVALID_ARGUMENT;
+  if (!aligned16(out->planes)) return APT_ERR_INVALID_ARGUMENT;
+  out->rows = rows;
+  out->k = k;
+  out->k_words = (int32_t)(kpad_of(k) / 32);
+  out->bits = bits;
+  apt::PackArgs p;
+  p.codes = codes;
+  p.ld = ld;
+  p.rows = rows;
+  p.k = k;
+  p.k_words = out->k_words;
+  p.enc = (int32_t)enc;
+  p.planes = out->planes;
+  p.plane_stride = (int64_t)rows * out->k_words;
+  p.row_sum = out->row_sum;
+  p.range_error = range_error;
+  cudaError_t err = apt::launch_pack(p, bits, reinterpret_cast<cudaStream_t>(stream));
+  return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+}
+
+apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, apt_config* out) {
+  if (!out || M <= 0 || N <= 0 || K <= 0 || wbits < 1 || wbits > 8 || abits < 1 || abits > 8)
+    return APT_ERR_INVALID_ARGUMENT;
+  if (!bound_ok(K, wbits, abits)) return APT_ERR_UNSUPPORTED;
+  std::memset(out, 0, sizeof(*out));
+  const int kw = (int)(kpad_of(K) / 32);
+  out->kernel = APT_KERNEL_MMA_SPLITK;
+  out->w_digit = wbits;
+  out->a_digit = abits;
+  out->bm = 64;
+  out->bk = 256;
+  out->stages = 2;
+  out->cta_pair = 0;
+  out->bn = M <= 8 ? 8 : M <= 16 ? 16 : M <= 32 ? 32 : 64;
+  // split-K so that the grid holds >= 4 CTAs per SM (HBM latency hiding for decode shapes),
+  // each split covering at least one 256-element iteration; cluster size <= 8 (portable)
+  const int64_t tiles = (int64_t)ceil_div(N, 64) * ceil_div(M, out->bn);
+  int split = (int)((4 * kNumSMs + tiles - 1) / tiles);
+  if (split > 8) split = 8;
+  if (split > kw / 8) split = kw / 8;
+  if (split < 1) split = 1;
+  out->split_k = split;
+  return APT_OK;
+}
+
+size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
+  (void)cfg; (void)M; (void)N; (void)K;
+  return 0;
+}
+
+apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, const apt_packed* W,
+                    const apt_packed* A, const apt_scales* scales, apt_out_kind kind, apt_layout layout,
+                    void* out, int64_t ldo, const apt_config* cfg, void* workspace, size_t ws_bytes,
+                    void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || wbits < 1 || wbits > 8 || abits < 1 || abits > 8 || !out)
+    return APT_ERR_INVALID_ARGUMENT;
+  apt_status st = validate_packed(W, N, K, wbits);
+  if (st != APT_OK) return st;
+  st = validate_packed(A, M, K, abits);
+  if (st != APT_OK) return st;
+  if (kind != APT_OUT_I32_SIGNED && kind != APT_OUT_I32_BIPOLAR && kind != APT_OUT_F16_SCALED)
+    return APT_ERR_INVALID_ARGUMENT;
+  if (layout != APT_LAYOUT_ROW && layout != APT_LAYOUT_COL) return APT_ERR_INVALID_ARGUMENT;
+  if (layout == APT_LAYOUT_ROW ? ldo < N : ldo < M) return APT_ERR_INVALID_ARGUMENT;
+  if (kind == APT_OUT_F16_SCALED && (!scales || !scales->w_scale)) return APT_ERR_INVALID_ARGUMENT;
+  if (!bound_ok(K, wbits, abits)) return APT_ERR_UNSUPPORTED;
+  apt_config c;
+  if (cfg) {
+    c = *cfg;
+  } else {
+    st = apt_select_config(M, N, K, wbits, abits, &c);
+    if (st != APT_OK) return st;
+  }
+  st = validate_config(&c, M, N, K, wbits, abits);
+  if (st != APT_OK) return st;
+  const size_t need = apt_gemm_workspace_bytes(&c, M, N, K);
+  if (need > 0 && (!workspace || ws_bytes < need)) return APT_ERR_WORKSPACE;
+
+  apt::EpilogueArgs e;
+  e.w_rowsum = W->row_sum;
+  e.a_rowsum = A->row_sum;
+  e.w_scale = scales ? scales->w_scale : nullptr;
+  e.a_scale = scales ? scales->a_scale : nullptr;
+  e.out = out;
+  e.ldo = ldo;
+  e.kind = (int32_t)kind;
+  e.layout = (int32_t)layout;
+  e.M = M;
+  e.N = N;
+  e.K = K;
+  e.kpad = (int32_t)kpad_of(K);
+  e.h_w = 1 << (wbits - 1);
+  e.h_a = 1 << (abits - 1);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+
+  if (c.kernel == APT_KERNEL_MMA_SPLITK) {
+    apt::MmaArgs p;
+    p.wp = W->planes;
+    p.w_pstride = (int64_t)N * W->k_words;
+    p.ap = A->planes;
+    p.a_pstride = (int64_t)M * A->k_words;
+    p.k_words = W->k_words;
+    p.abits = abits;
+    const int per = ceil_div(W->k_words, c.split_k);
+    p.kw_per_split = ((per + 7) / 8) * 8;
+    p.e = e;
+    const int split = ceil_div(W->k_words, p.kw_per_split);
+    cudaError_t err = apt::launch_gemm_mma(p, wbits, c.bn, split, s);
+    return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+  }
+  return APT_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

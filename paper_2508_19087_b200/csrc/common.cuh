@@ -1,0 +1,155 @@
+// common.cuh — device helpers shared by the APT kernels (product path only; the CPU oracle
+// under oracle/ shares nothing with this file).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace apt {
+
+// ---------------------------------------------------------------------------------------------
+// Operand rebuild: bit-planes -> full-width unsigned digits (the "shift" half of the paper's
+// shift-add recovery, folded onto the operands).
+//
+// Input : Q plane words w[i] (i = plane = bit significance), each holding bit i of the
+//         bipolar pattern u = x + 2^(Q-1) of 32 consecutive K elements (§4.1 Step 2).
+// Output: 8 registers of 4 bytes; every byte is one element's u in [0, 2^Q), i.e. the digit
+//         sum_i 2^i u_i.  The 32 elements land in the 32 byte slots through a fixed bijection
+//         (a butterfly bit transpose).  The K order inside a word is irrelevant to the GEMM as long
+//         as BOTH operands go through this same function for the same word (sum over K commutes),
+//         so the exported packed format stays canonical while the kernel uses the cheapest order.
+//
+// Cost: Q=1 15 ops, Q=2 18, Q=4 28, Q=8 48 LOP3/SHF per 32 elements.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void bf_pair(uint32_t lo, uint32_t hi, int s, uint32_t m, uint32_t& a, uint32_t& b) {
+  // a: even fields of lo in the low half, even fields of hi in the high half (field width s)
+  // b: odd fields likewise.  m = mask of the low s bits of every 2s-bit field.
+  a = (lo & m) | ((hi << s) & ~m);
+  b = ((lo >> s) & m) | (hi & ~m);
+}
+
+template <int Q>
+__device__ __forceinline__ void rebuild8(const uint32_t* w, uint32_t (&o)[8]) {
+  static_assert(Q >= 1 && Q <= 8, "bits");
+  if constexpr (Q == 1) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (w[0] >> j) & 0x01010101u;
+  } else if constexpr (Q == 2) {
+    uint32_t e, f;
+    bf_pair(w[0], w[1], 1, 0x55555555u, e, f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      o[j] = (e >> (2 * j)) & 0x03030303u;
+      o[4 + j] = (f >> (2 * j)) & 0x03030303u;
+    }
+  } else if constexpr (Q <= 4) {
+    const uint32_t w3 = (Q == 4) ? w[3] : 0u;
+    uint32_t e01, f01, e23, f23, g[4];
+    bf_pair(w[0], w[1], 1, 0x55555555u, e01, f01);
+    bf_pair(w[2], w3, 1, 0x55555555u, e23, f23);
+    bf_pair(e01, e23, 2, 0x33333333u, g[0], g[1]);
+    bf_pair(f01, f23, 2, 0x33333333u, g[2], g[3]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      o[2 * c] = g[c] & 0x0F0F0F0Fu;
+      o[2 * c + 1] = (g[c] >> 4) & 0x0F0F0F0Fu;
+    }
+  } else {
+    const uint32_t w5 = (Q >= 6) ? w[5] : 0u;
+    const uint32_t w6 = (Q >= 7) ? w[6] : 0u;
+    const uint32_t w7 = (Q >= 8) ? w[7] : 0u;
+    uint32_t e01, f01, e23, f23, e45, f45, e67, f67, g[8];
+    bf_pair(w[0], w[1], 1, 0x55555555u, e01, f01);
+    bf_pair(w[2], w[3], 1, 0x55555555u, e23, f23);
+    bf_pair(w[4], w5, 1, 0x55555555u, e45, f45);
+    bf_pair(w6, w7, 1, 0x55555555u, e67, f67);
+    bf_pair(e01, e23, 2, 0x33333333u, g[0], g[1]);
+    bf_pair(e45, e67, 2, 0x33333333u, g[2], g[3]);
+    bf_pair(f01, f23, 2, 0x33333333u, g[4], g[5]);
+    bf_pair(f45, f67, 2, 0x33333333u, g[6], g[7]);
+    bf_pair(g[0], g[2], 4, 0x0F0F0F0Fu, o[0], o[1]);
+    bf_pair(g[1], g[3], 4, 0x0F0F0F0Fu, o[2], o[3]);
+    bf_pair(g[4], g[6], 4, 0x0F0F0F0Fu, o[4], o[5]);
+    bf_pair(g[5], g[7], 4, 0x0F0F0F0Fu, o[6], o[7]);
+  }
+}
+
+// Runtime-width dispatch (used where the width is not a template parameter, e.g. token rebuild).
+__device__ __forceinline__ void rebuild8_rt(const uint32_t* w, int q, uint32_t (&o)[8]) {
+  switch (q) {
+    case 1: rebuild8<1>(w, o); break;
+    case 2: rebuild8<2>(w, o); break;
+    case 3: rebuild8<3>(w, o); break;
+    case 4: rebuild8<4>(w, o); break;
+    case 5: rebuild8<5>(w, o); break;
+    case 6: rebuild8<6>(w, o); break;
+    case 7: rebuild8<7>(w, o); break;
+    default: rebuild8<8>(w, o); break;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Epilogue arithmetic (reading Q1/Q10; SURVEY §8c identities I2/I3).
+// The kernels accumulate U = sum_{k<Kpad} u_a u_w over unsigned digits u = x + h (h = 2^(n-1)).
+// Since pads are signed code 0 (u = h):
+//     Y  = U - h_w * RA[m] - h_a * RW[n] - Kpad * h_a * h_w      (signed product)
+//     Y' = 4Y + 2 RA[m] + 2 RW[n] + K                           (bipolar product)
+// evaluated modulo 2^32 (the true values fit in int32 by the Q8 bound, so wraparound is exact).
+// ---------------------------------------------------------------------------------------------
+struct EpilogueArgs {
+  const int32_t* w_rowsum;  // RW[N]
+  const int32_t* a_rowsum;  // RA[M]
+  const float* w_scale;     // [N]
+  const float* a_scale;     // [M] or null
+  void* out;
+  int64_t ldo;
+  int32_t kind;             // apt_out_kind
+  int32_t layout;           // apt_layout
+  int32_t M, N, K, kpad;
+  int32_t h_w, h_a;         // 2^(wbits-1), 2^(abits-1)
+};
+
+__device__ __forceinline__ void epilogue_store(const EpilogueArgs& e, int m, int n, uint32_t U) {
+  const uint32_t ra = (uint32_t)__ldg(e.a_rowsum + m);
+  const uint32_t rw = (uint32_t)__ldg(e.w_rowsum + n);
+  const uint32_t y = U - (uint32_t)e.h_w * ra - (uint32_t)e.h_a * rw -
+                     (uint32_t)e.kpad * (uint32_t)e.h_a * (uint32_t)e.h_w;
+  const int64_t off = e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m;
+  if (e.kind == 0) {
+    reinterpret_cast<int32_t*>(e.out)[off] = (int32_t)y;
+  } else if (e.kind == 1) {
+    const uint32_t yb = 4u * y + 2u * ra + 2u * rw + (uint32_t)e.K;
+    reinterpret_cast<int32_t*>(e.out)[off] = (int32_t)yb;
+  } else {
+    float v = (float)(int32_t)y * __ldg(e.w_scale + n);
+    if (e.a_scale) v = v * __ldg(e.a_scale + m);
+    unsigned short h;
+    asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(v));
+    reinterpret_cast<unsigned short*>(e.out)[off] = h;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Small PTX wrappers
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_dsmem_u32(uint32_t local_smem_addr, uint32_t rank) {
+  uint32_t remote, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_smem_addr), "r"(rank));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+}  // namespace apt

@@ -1,0 +1,149 @@
+// pack.cu — INT -> bipolar-INT bit-plane packing on the device (§4.1 Steps 1-3).
+//
+// One CTA per matrix row; each thread owns one 32-bit output word position (32 consecutive K
+// elements) at a time and loads those 32 codes as two 16-byte vectors (a warp reads 1 KB of
+// contiguous codes).  Per 4-byte group of codes:
+//   signed -> offset bits   u = x + 2^(n-1) mod 2^n, i.e. the sign-bit flip of P:202, done
+//                           bytewise without cross-byte carries;
+//   plane i nibble          ((u >> i) & 0x01010101) * 0x01020408 >> 24 gathers bit i of the
+//                           four bytes into 4 consecutive bits;
+// and the eight nibbles of a plane form the output word (element c -> bit c%32, LSB first).
+// Row sums of the signed codes use dp4a; the CTA reduces them without atomics.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace apt {
+
+
+// bytewise: signed codes (4 per word) -> offset digits u (4 per word), modulo 2^BITS
+template <int BITS>
+__device__ __forceinline__ uint32_t to_offset4(uint32_t v) {
+  if constexpr (BITS == 8) {
+    return v ^ 0x80808080u;
+  } else {
+    constexpr uint32_t h = 1u << (BITS - 1);
+    constexpr uint32_t mask = (1u << BITS) - 1u;
+    // (x & 0x7F) + h < 256 never carries into the next byte; mod 2^BITS it equals x + h since 2^BITS | 128
+    return ((v & 0x7F7F7F7Fu) + h * 0x01010101u) & (mask * 0x01010101u);
+  }
+}
+
+// bytewise: offset digits -> sign-extended signed codes (used to detect out-of-range inputs)
+template <int BITS>
+__device__ __forceinline__ uint32_t from_offset4(uint32_t u) {
+  if constexpr (BITS == 8) {
+    return u ^ 0x80808080u;
+  } else {
+    constexpr uint32_t h = 1u << (BITS - 1);
+    const uint32_t x = u ^ (h * 0x01010101u);                   // n-bit two's complement pattern
+    const uint32_t s = (x >> (BITS - 1)) & 0x01010101u;         // sign bit of every byte
+    return x | (s * (0x100u - 2u * h));                          // sign-extend (no cross-byte carry)
+  }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(128) pack_kernel(PackArgs p) {
+  const int r = blockIdx.x;
+  const int8_t* row = p.codes + (int64_t)r * p.ld;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0);
+  int sum = 0;
+  for (int w = threadIdx.x; w < p.k_words; w += blockDim.x) {
+    const int c0 = w * 32;
+    uint32_t v[8];
+    if (vec_ok && c0 + 32 <= p.k) {
+      const uint4 lo = __ldg(reinterpret_cast<const uint4*>(row + c0));
+      const uint4 hi = __ldg(reinterpret_cast<const uint4*>(row + c0 + 16));
+      v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
+      v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int c = c0 + 4 * j + b;
+          const uint32_t byte = (c < p.k) ? (uint32_t)(uint8_t)row[c] : 0u;  // pad = signed code 0
+          word |= byte << (8 * b);
+        }
+        v[j] = word;
+      }
+      if (p.enc == 1) {
+        // bipolar pads must also be neutral: pad positions hold x' = 1 (signed 0) after conversion
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (c0 + 4 * j + b >= p.k) v[j] |= 1u << (8 * b);
+      }
+    }
+    uint32_t u[8];
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t x = v[j];
+      if (p.enc == 1) {
+        // bipolar x' (odd) -> signed x = (x' - 1) / 2 = x' >> 1 (arithmetic, bytewise)
+        bad |= (x & 0x01010101u) != 0x01010101u;
+        x = ((x >> 1) & 0x7F7F7F7Fu) | (x & 0x80808080u);
+      }
+      u[j] = to_offset4<BITS>(x);
+      bad |= from_offset4<BITS>(u[j]) != x;
+      sum = __dp4a((int)x, 0x01010101, sum);
+    }
+    if (bad && p.range_error) {
+      for (int c = c0; c < c0 + 32 && c < p.k; ++c) {
+        int x = row[c];
+        bool ok;
+        if (p.enc == 1) {
+          ok = (x & 1) && x >= -((1 << BITS) - 1) && x <= (1 << BITS) - 1;
+          x = x >> 1;
+        } else {
+          ok = x >= -(1 << (BITS - 1)) && x <= (1 << (BITS - 1)) - 1;
+        }
+        if (!ok) {
+          const int64_t li = (int64_t)r * p.k + c + 1;
+          atomicCAS(p.range_error, 0, li > 0x7FFFFFFF ? 0x7FFFFFFF : (int)li);
+          break;
+        }
+      }
+    }
+    // planes: bit i of every element, element c -> bit c % 32 (LSB first)
+    uint32_t* dst = p.planes + (int64_t)r * p.k_words + w;
+#pragma unroll
+    for (int i = 0; i < BITS; ++i) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t nib = (((u[j] >> i) & 0x01010101u) * 0x01020408u) >> 24;
+        word |= nib << (4 * j);
+      }
+      dst[(int64_t)i * p.plane_stride] = word;
+    }
+  }
+  // CTA reduction of the row sum (pads contribute 0)
+  __shared__ int red[4];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) p.row_sum[r] = red[0] + red[1] + red[2] + red[3];
+}
+
+cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream) {
+  dim3 grid(p.rows), block(128);
+  switch (bits) {
+    case 1: pack_kernel<1><<<grid, block, 0, stream>>>(p); break;
+    case 2: pack_kernel<2><<<grid, block, 0, stream>>>(p); break;
+    case 3: pack_kernel<3><<<grid, block, 0, stream>>>(p); break;
+    case 4: pack_kernel<4><<<grid, block, 0, stream>>>(p); break;
+    case 5: pack_kernel<5><<<grid, block, 0, stream>>>(p); break;
+    case 6: pack_kernel<6><<<grid, block, 0, stream>>>(p); break;
+    case 7: pack_kernel<7><<<grid, block, 0, stream>>>(p); break;
+    default: pack_kernel<8><<<grid, block, 0, stream>>>(p); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace apt

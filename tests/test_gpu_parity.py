@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bars: packed planes and row sums bit-exact; int32 outputs (signed and
+bipolar) bit-exact; fp16-scaled output within 1e-3 relative of the fp64 oracle.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import apt_oracle as O
+from oracle import c_gemm_i64
+from synth import config_seed, log_uniform_scales, signed_codes
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2508_19087_b200")
+
+DEV = "cuda:0"
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _pack_both(a_codes, abits, w_codes, wbits):
+    A = P.pack(_dev(a_codes), abits)
+    W = P.pack(_dev(w_codes), wbits)
+    return A, W
+
+
+# ----------------------------------------------------------------------------- pack (T6)
+
+@pytest.mark.parametrize("bits", range(1, 9))
+@pytest.mark.parametrize("rows,k", [(1, 1), (3, 31), (5, 33), (7, 255), (2, 257), (17, 4096), (3, 11008)])
+def test_pack_matches_oracle(bits, rows, k):
+    codes = signed_codes(rows, k, bits, seed=31 * bits + k + rows)
+    got = P.pack(_dev(codes), bits)
+    planes, rs = O.pack_planes(codes, bits)
+    torch.cuda.synchronize()
+    assert np.array_equal(got.planes.cpu().numpy().view(np.uint32), planes)
+    assert np.array_equal(got.row_sum.cpu().numpy().astype(np.int64), rs)
+
+
+@pytest.mark.parametrize("bits", range(1, 8))
+def test_pack_bipolar_encoding(bits):
+    codes = signed_codes(9, 300, bits, seed=bits)
+    bip = (2 * codes.astype(np.int64) + 1).astype(np.int8)
+    got = P.pack(_dev(bip), bits, encoding="bipolar")
+    planes, rs = O.pack_planes(codes, bits)
+    assert np.array_equal(got.planes.cpu().numpy().view(np.uint32), planes)
+    assert np.array_equal(got.row_sum.cpu().numpy().astype(np.int64), rs)
+
+
+def test_pack_strided_rows():
+    codes = signed_codes(6, 500, 3, seed=5)
+    big = np.zeros((6, 777), dtype=np.int8)
+    big[:, :500] = codes
+    t = _dev(big)[:, :500]
+    got = P.pack(t, 3)
+    planes, _ = O.pack_planes(codes, 3)
+    assert np.array_equal(got.planes.cpu().numpy().view(np.uint32), planes)
+
+
+def test_pack_range_error_flag():
+    codes = signed_codes(4, 100, 3, seed=9)
+    codes[2, 17] = 5  # outside [-4, 3]
+    flag = torch.zeros(1, dtype=torch.int32, device=DEV)
+    P.pack(_dev(codes), 3, range_error=flag)
+    assert int(flag.item()) == 2 * 100 + 17 + 1
+    flag.zero_()
+    P.pack(_dev(signed_codes(4, 100, 3, seed=9)), 3, range_error=flag)
+    assert int(flag.item()) == 0
+
+
+# ----------------------------------------------------------------------------- GEMM (T7)
+
+def _check_gemm(a, abits, w, wbits, config=None, layouts=("row",)):
+    A, W = _pack_both(a, abits, w, wbits)
+    y = O.gemm_signed(a, w)
+    yb = O.gemm_bipolar(a, abits, w, wbits) if a.shape[1] * a.shape[0] * w.shape[0] < 3e6 else \
+        4 * y + 2 * a.astype(np.int64).sum(1)[:, None] + 2 * w.astype(np.int64).sum(1)[None, :] + a.shape[1]
+    for lay in layouts:
+        got = P.gemm(W, A, out_kind="i32", layout=lay, config=config).cpu().numpy()
+        got = got if lay == "row" else got.T
+        assert np.array_equal(got.astype(np.int64), y), f"signed mismatch ({lay})"
+        gotb = P.gemm(W, A, out_kind="bipolar", layout=lay, config=config).cpu().numpy()
+        gotb = gotb if lay == "row" else gotb.T
+        assert np.array_equal(gotb.astype(np.int64), yb), f"bipolar mismatch ({lay})"
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_config1_w2a2(seed):
+    """BASELINE configs[0]: W2A2, M=16, N=K=256."""
+    a = signed_codes(16, 256, 2, seed=config_seed(0, 2, 2, seed))
+    w = signed_codes(256, 256, 2, seed=config_seed(0, 2, 2, seed) + 7)
+    _check_gemm(a, 2, w, 2, layouts=("row", "col"))
+
+
+def test_random_set():
+    """SPEC acceptance 1: random M, N, K in [1,300], p, q in [1,8] (200 instances)."""
+    rng = np.random.default_rng(2024)
+    for t in range(200):
+        m, n, k = (int(v) for v in rng.integers(1, 301, size=3))
+        pa, pw = (int(v) for v in rng.integers(1, 9, size=2))
+        a = signed_codes(m, k, pa, seed=10 * t)
+        w = signed_codes(n, k, pw, seed=10 * t + 1)
+        _check_gemm(a, pa, w, pw)
+
+
+@pytest.mark.parametrize("pa,pw", [(p, q) for p in range(1, 9) for q in range(1, 9)])
+def test_all_precisions_ragged(pa, pw):
+    """Every W_p x A_q combination on a shape with ragged M, N and K tails."""
+    a = signed_codes(37, 700, pa, seed=100 * pa + pw)
+    w = signed_codes(131, 700, pw, seed=100 * pw + pa + 5)
+    _check_gemm(a, pa, w, pw)
+
+
+def test_extreme_codes_overflow_edge():
+    """All-minimum codes at the largest K the int32 bound allows for W8A8 (|Y| = K * 2^14)."""
+    k = 33024
+    a = np.full((3, k), -128, dtype=np.int8)
+    w = np.full((70, k), -128, dtype=np.int8)
+    _check_gemm(a, 8, w, 8)
+    a[:, ::2] = 127
+    _check_gemm(a, 8, w, 8)
+
+
+def test_bound_rejected():
+    a = signed_codes(2, 33025, 8, seed=1)
+    A, W = _pack_both(a, 8, a, 8)
+    with pytest.raises(RuntimeError, match="UNSUPPORTED"):
+        P.gemm(W, A)
+
+
+@pytest.mark.parametrize("bn,split", [(8, 1), (16, 2), (32, 3), (64, 8), (8, 8)])
+def test_config_invariance(bn, split):
+    """any legal configuration gives identical bits."""
+    a = signed_codes(20, 4096, 4, seed=3)
+    w = signed_codes(200, 4096, 3, seed=4)
+    cfg = P.select_config(20, 200, 4096, 3, 4)
+    cfg.update(bn=bn, split_k=split)
+    _check_gemm(a, 4, w, 3, config=cfg)
+
+
+# ----------------------------------------------------------------------------- fp16 epilogue (T9)
+
+@pytest.mark.parametrize("pa,pw,m", [(2, 2, 16), (4, 4, 8), (8, 8, 5), (4, 3, 1)])
+def test_f16_scaled(pa, pw, m):
+    n, k = 300, 1000
+    a = signed_codes(m, k, pa, seed=7 + pa)
+    w = signed_codes(n, k, pw, seed=8 + pw)
+    ws = log_uniform_scales(n, -10, -6, seed=1)
+    as_ = log_uniform_scales(m, -6, -2, seed=2)
+    A, W = _pack_both(a, pa, w, pw)
+    ref = O.scale_fp64(O.gemm_signed(a, w), ws, as_)
+    for lay in ("row", "col"):
+        got = P.gemm(W, A, out_kind="f16", layout=lay, w_scale=_dev(ws), a_scale=_dev(as_)).cpu().numpy()
+        got = (got if lay == "row" else got.T).astype(np.float64)
+        err = np.abs(got - ref)
+        assert (err <= 1e-3 * np.abs(ref) + 2.0 ** -24).all()
+    got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws)).cpu().numpy().astype(np.float64)
+    ref1 = O.scale_fp64(O.gemm_signed(a, w), ws, None)
+    assert (np.abs(got - ref1) <= 1e-3 * np.abs(ref1) + 2.0 ** -24).all()
+
+
+# ----------------------------------------------------------------------------- full-size configs (T8)
+
+LLAMA7B = [(4096, 4096), (11008, 4096), (4096, 11008)]
+
+
+@pytest.mark.parametrize("n,k", LLAMA7B)
+@pytest.mark.parametrize("m", [1, 8, 16])
+@pytest.mark.parametrize("pw,pa", [(1, 2), (2, 2), (3, 4), (4, 4)])
+def test_llama7b_decode_full(n, k, m, pw, pa):
+    """BASELINE configs[1] at full size in the bench's launch configuration (selector default),
+    every output element vs the C int64 oracle."""
+    a = signed_codes(m, k, pa, seed=config_seed(1, pw, pa))
+    w = signed_codes(n, k, pw, seed=config_seed(1, pw, pa) + 1)
+    A, W = _pack_both(a, pa, w, pw)
+    got = P.gemm(W, A).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, c_gemm_i64(a, w))
+
+
+@pytest.mark.parametrize("n,k", LLAMA7B)
+@pytest.mark.parametrize("pw,pa", [(2, 8), (4, 4)])
+def test_llama7b_prefill_sampled(n, k, pw, pa):
+    """BASELINE configs[2] (M=2048) at full size: 16 sampled token rows vs the C oracle, plus a
+    property that holds at any size (row sums of Y = A . (sum of W rows))."""
+    m = 2048
+    a = signed_codes(m, k, pa, seed=config_seed(2, pw, pa))
+    w = signed_codes(n, k, pw, seed=config_seed(2, pw, pa) + 1)
+    A, W = _pack_both(a, pa, w, pw)
+    got = P.gemm(W, A).cpu().numpy().astype(np.int64)
+    rows = np.random.default_rng(0).choice(m, 16, replace=False)
+    assert np.array_equal(got[rows], c_gemm_i64(a[rows], w))
+    wsum = w.astype(np.int64).sum(0)
+    assert np.array_equal(got.sum(1), a.astype(np.int64) @ wsum)
