@@ -15,6 +15,7 @@ N > 1 (torchrun): tensor parallel N-split of every linear's weight rows, each ra
 --impl reference: the CPU oracle (C int64 GEMM, oracle/) on host cores, rank 0 only.
 """
 import argparse
+import faulthandler
 import json
 import os
 import statistics
@@ -39,6 +40,10 @@ def kpad(k):
 def alg_bytes(m, n, k, wb, ab):
     """Algorithmic HBM bytes of one GEMM launch: packed W + packed A planes, row sums, scales, fp16 out."""
     return n * kpad(k) * wb // 8 + m * kpad(k) * ab // 8 + 8 * (m + n) + 2 * m * n
+
+
+def log(msg):
+    print(f"[bench] {msg}", file=sys.stderr, flush=True)
 
 
 def parse():
@@ -81,12 +86,13 @@ class ClockSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
-            import torch
-            try:
-                bus = torch.cuda.get_device_properties(device_index).pci_bus_id
-                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
-            except Exception:
-                self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            phys = device_index
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            if vis:
+                ids = [v.strip() for v in vis.split(",")]
+                if device_index < len(ids) and ids[device_index].isdigit():
+                    phys = int(ids[device_index])
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
             self.nv = pynvml
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
@@ -179,6 +185,7 @@ def run_reference(args, rank, world):
 # ----------------------------------------------------------------------------- GPU arm
 
 def main():
+    faulthandler.enable()
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -200,6 +207,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    log("setup")
     sampler = ClockSampler(local)
     sampler.start()
     stream = torch.cuda.Stream()
@@ -259,6 +267,7 @@ def main():
             if world > 1:
                 dist.all_gather_into_tensor(gathered[i], outs[i])
 
+    log("eager warm steps")
     # ---- capture instrumented step graphs (external timing events around every GEMM launch)
     n_graphs = 2 * max(1, min(8, args.steps // 2))
     graphs, events = [], []
@@ -288,6 +297,7 @@ def main():
         else:
             step(j % 2, events[j % n_graphs])
 
+    log(f"graphs={use_graphs}; warmup")
     for j in range(args.warmup):
         run(j)
     barrier()
@@ -348,6 +358,7 @@ def main():
             "per_precision_gemm_tops": per_prec, "per_m": per_m,
             "weight_pack": {"ms": round(wpack_ms, 3), "GB/s": round(wpack_bytes / (wpack_ms * 1e-3) / 1e9, 1)}}
 
+    log("baselines")
     if not args.no_baselines:
         line.update(baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout,
                               value, barrier))

@@ -41,6 +41,11 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
     if (c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
     return APT_OK;
   }
+  if (c->kernel == APT_KERNEL_TC) {
+    if (c->bm != 128 || c->bk != 128 || (c->bn != 128 && c->bn != 256)) return APT_ERR_UNSUPPORTED;
+    if (c->stages < 2 || c->stages > 6 || c->split_k != 1 || c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
+    return APT_OK;
+  }
   return APT_ERR_UNSUPPORTED;
 }
 
@@ -98,9 +103,20 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
   if (!bound_ok(K, wbits, abits)) return APT_ERR_UNSUPPORTED;
   std::memset(out, 0, sizeof(*out));
   const int kw = (int)(kpad_of(K) / 32);
-  out->kernel = APT_KERNEL_MMA_SPLITK;
   out->w_digit = wbits;
   out->a_digit = abits;
+  if (M > 64) {
+    // prefill: tcgen05 kind::i8, 128 weight rows x 128 tokens per CTA, two CTAs per SM
+    out->kernel = APT_KERNEL_TC;
+    out->bm = 128;
+    out->bn = 128;
+    out->bk = 128;
+    out->stages = apt::tc_stages(wbits, out->bn);
+    out->split_k = 1;
+    out->cta_pair = 0;
+    return APT_OK;
+  }
+  out->kernel = APT_KERNEL_MMA_SPLITK;
   out->bm = 64;
   out->bk = 256;
   out->stages = 2;
@@ -118,7 +134,9 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
 }
 
 size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
-  (void)cfg; (void)M; (void)N; (void)K;
+  (void)N;
+  if (!cfg || M <= 0 || K <= 0) return 0;
+  if (cfg->kernel == APT_KERNEL_TC) return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
   return 0;
 }
 
@@ -180,6 +198,19 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
     p.e = e;
     const int split = ceil_div(W->k_words, p.kw_per_split);
     cudaError_t err = apt::launch_gemm_mma(p, wbits, c.bn, split, s);
+    return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+  }
+  if (c.kernel == APT_KERNEL_TC) {
+    if (!aligned16(workspace)) return APT_ERR_WORKSPACE;
+    apt::TcArgs p;
+    p.wp = W->planes;
+    p.w_pstride = (int64_t)N * W->k_words;
+    p.ap = A->planes;
+    p.a_pstride = (int64_t)M * A->k_words;
+    p.k_words = W->k_words;
+    p.abits = abits;
+    p.e = e;
+    cudaError_t err = apt::launch_gemm_tc(p, wbits, c.bn, c.stages, workspace, s);
     return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   return APT_ERR_UNSUPPORTED;

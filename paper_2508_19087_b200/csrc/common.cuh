@@ -18,34 +18,27 @@ namespace apt {
 //         as BOTH operands go through this same function for the same word (sum over K commutes),
 //         so the exported packed format stays canonical while the kernel uses the cheapest order.
 //
-// Cost: Q=1 15 ops, Q=2 18, Q=4 28, Q=8 48 LOP3/SHF per 32 elements.
+// Cost (after constant folding): about 20 ops for Q <= 2, 28 for Q = 4, 48 for Q = 8 per 32 elements.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void bf_pair(uint32_t lo, uint32_t hi, int s, uint32_t m, uint32_t& a, uint32_t& b) {
+__host__ __device__ __forceinline__ void bf_pair(uint32_t lo, uint32_t hi, int s, uint32_t m, uint32_t& a, uint32_t& b) {
   // a: even fields of lo in the low half, even fields of hi in the high half (field width s)
   // b: odd fields likewise.  m = mask of the low s bits of every 2s-bit field.
   a = (lo & m) | ((hi << s) & ~m);
   b = ((lo >> s) & m) | (hi & ~m);
 }
 
+// The element -> byte-slot bijection is the SAME for every Q (planes >= Q are zero and the
+// compiler folds them away), so operands of different widths agree on the K order.
 template <int Q>
-__device__ __forceinline__ void rebuild8(const uint32_t* w, uint32_t (&o)[8]) {
+__host__ __device__ __forceinline__ void rebuild8(const uint32_t* w, uint32_t (&o)[8]) {
   static_assert(Q >= 1 && Q <= 8, "bits");
-  if constexpr (Q == 1) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = (w[0] >> j) & 0x01010101u;
-  } else if constexpr (Q == 2) {
-    uint32_t e, f;
-    bf_pair(w[0], w[1], 1, 0x55555555u, e, f);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      o[j] = (e >> (2 * j)) & 0x03030303u;
-      o[4 + j] = (f >> (2 * j)) & 0x03030303u;
-    }
-  } else if constexpr (Q <= 4) {
-    const uint32_t w3 = (Q == 4) ? w[3] : 0u;
+  if constexpr (Q <= 4) {
+    const uint32_t w1 = (Q >= 2) ? w[1] : 0u;
+    const uint32_t w2 = (Q >= 3) ? w[2] : 0u;
+    const uint32_t w3 = (Q >= 4) ? w[3] : 0u;
     uint32_t e01, f01, e23, f23, g[4];
-    bf_pair(w[0], w[1], 1, 0x55555555u, e01, f01);
-    bf_pair(w[2], w3, 1, 0x55555555u, e23, f23);
+    bf_pair(w[0], w1, 1, 0x55555555u, e01, f01);
+    bf_pair(w2, w3, 1, 0x55555555u, e23, f23);
     bf_pair(e01, e23, 2, 0x33333333u, g[0], g[1]);
     bf_pair(f01, f23, 2, 0x33333333u, g[2], g[3]);
 #pragma unroll
@@ -74,7 +67,7 @@ __device__ __forceinline__ void rebuild8(const uint32_t* w, uint32_t (&o)[8]) {
 }
 
 // Runtime-width dispatch (used where the width is not a template parameter, e.g. token rebuild).
-__device__ __forceinline__ void rebuild8_rt(const uint32_t* w, int q, uint32_t (&o)[8]) {
+__host__ __device__ __forceinline__ void rebuild8_rt(const uint32_t* w, int q, uint32_t (&o)[8]) {
   switch (q) {
     case 1: rebuild8<1>(w, o); break;
     case 2: rebuild8<2>(w, o); break;

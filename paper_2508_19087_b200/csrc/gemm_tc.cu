@@ -1,0 +1,404 @@
+// gemm_tc.cu — APT W_p x A_q GEMM on the 5th-generation tensor cores (tcgen05, kind::i8) for
+// prefill-sized token counts.
+//
+//   D[128 weight rows x BN tokens] (s32, TMEM) += A[128 x K] (u8 digits, TMEM) . B[BN x K]^T (u8, SMEM)
+//
+// Per CTA (8 warps, one 128 x BN output tile, 2 CTAs per SM at BN = 128):
+//   warp 0      TMA producer: per 128-element K step, one 3-D TMA box of ALL weight planes
+//               ({4 words, 128 rows, wbits planes}: the paper's concatenated "unified matrix", §4.1
+//               Step 3, moved with a single command) + one 2-D box of token digits
+//               (128 B x BN rows, 128-byte swizzle) into a `stages`-deep shared-memory ring.
+//   warp 1      MMA issuer (one thread): 4 x tcgen05.mma.cta_group::1.kind::i8 (M=128, N=BN, K=32)
+//               per K step, A from TMEM, B from a shared-memory descriptor; tcgen05.commit frees
+//               the ring slots.
+//   warp 2      TMEM allocator.
+//   warps 4..7  converters, then epilogue.  Thread = weight row (= TMEM lane).  Per K step each
+//               thread reads its row's wbits x 16 B of planes, rebuilds the 128 u8 digits with
+//               rebuild8() (the shift half of the shift-add recovery) and writes them to the
+//               TMEM A ring with tcgen05.st — the planes never leave the SM in any other form
+//               (recovery-oriented scheduling, §4.2).  After the last MMA they load the
+//               accumulator with tcgen05.ld and apply the rank-1 correction + scale (common.cuh).
+//
+// Token digits come from the per-call expand pre-pass (expand_tokens_kernel) which writes the
+// activation planes as u8 digits [M][Kpad] in the same within-word K order rebuild8() uses, so
+// both operands agree on K.
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace apt {
+
+constexpr int kTcBM = 128;       // weight rows per tile (MMA M)
+constexpr int kTcBK = 128;       // K elements per pipeline step
+constexpr int kTcAStages = 4;    // TMEM A ring depth (32 columns each)
+
+// ------------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// SMEM matrix descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart (SBO),
+// version 1 (sm_100), base offset 0 (stage buffers are 1024-byte aligned).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;             // LBO (unused for swizzled K-major) = 16 B
+  d |= (uint64_t)(1024 >> 4) << 32;   // SBO = 1024 B
+  d |= (uint64_t)1 << 46;             // version
+  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+  return d;
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------ pre-pass
+// Activation planes [abits][M][k_words] -> u8 digits [M][Kpad] in rebuild8() order.
+__global__ void __launch_bounds__(256) expand_tokens_kernel(const uint32_t* __restrict__ ap, int64_t a_pstride,
+                                                            int32_t M, int32_t k_words, int32_t abits,
+                                                            uint8_t* __restrict__ ws) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)M * k_words) return;
+  uint32_t w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = i < abits ? __ldg(ap + (int64_t)i * a_pstride + idx) : 0u;
+  uint32_t d[8];
+  rebuild8_rt(w, abits, d);
+  uint4* dst = reinterpret_cast<uint4*>(ws + idx * 32);
+  dst[0] = make_uint4(d[0], d[1], d[2], d[3]);
+  dst[1] = make_uint4(d[4], d[5], d[6], d[7]);
+}
+
+// ------------------------------------------------------------------------------------ main kernel
+template <int WB, int BN, int STAGES>
+struct TcSmem {
+  static constexpr int kBBytes = BN * kTcBK;            // token digits per stage
+  static constexpr int kWBytes = WB * kTcBM * 16;       // weight planes per stage (4 words per row per plane)
+  static constexpr int kBOff = 0;
+  static constexpr int kWOff = STAGES * kBBytes;
+  static constexpr int kBarOff = kWOff + STAGES * kWBytes;
+  static constexpr int kNumBars = 2 * STAGES + 2 * kTcAStages + 1;
+  static constexpr int kTotal = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
+};
+
+template <int WB, int BN, int STAGES>
+__global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w,
+                                                         const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
+  using L = TcSmem<WB, BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sB = base + L::kBOff;
+  const uint32_t sW = base + L::kWOff;
+  const uint32_t bars = base + L::kBarOff;
+  auto full = [&](int s) { return bars + 8u * s; };
+  auto empty = [&](int s) { return bars + 8u * (STAGES + s); };
+  auto a_full = [&](int a) { return bars + 8u * (2 * STAGES + a); };
+  auto a_empty = [&](int a) { return bars + 8u * (2 * STAGES + kTcAStages + a); };
+  const uint32_t acc_full = bars + 8u * (2 * STAGES + 2 * kTcAStages);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::kBarOff + L::kNumBars * 8);
+  constexpr uint32_t kTmemCols = (BN + 32 * kTcAStages) <= 256 ? 256 : 512;
+  constexpr uint32_t kAcol0 = BN;  // A ring after the accumulator columns
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * kTcBM;   // weight rows
+  const int m0 = blockIdx.y * BN;      // tokens
+  const int nk = p.k_words / 4;        // 128-element K steps
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1 + 4);
+    }
+    for (int a = 0; a < kTcAStages; ++a) {
+      mbar_init(a_full(a), 4);
+      mbar_init(a_empty(a), 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_w) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_b) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      constexpr uint32_t kTx = L::kBBytes + L::kWBytes;
+      for (int ks = 0; ks < nk; ++ks) {
+        const int s = ks % STAGES;
+        const uint32_t ph = (ks / STAGES) & 1;
+        mbar_wait(empty(s), ph ^ 1);
+        mbar_expect_tx(full(s), kTx);
+        tma_load_2d(sB + s * L::kBBytes, &tm_b, full(s), ks * kTcBK, m0);
+        tma_load_3d(sW + s * L::kWBytes, &tm_w, full(s), ks * 4, n0, 0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = (2u << 4)                       // D = s32
+                                 | ((uint32_t)(BN >> 3) << 17)   // N
+                                 | ((uint32_t)(kTcBM >> 4) << 24);  // M ; A, B = u8, K-major
+      for (int ks = 0; ks < nk; ++ks) {
+        const int s = ks % STAGES;
+        const uint32_t ph = (ks / STAGES) & 1;
+        const int a = ks % kTcAStages;
+        const uint32_t pa = (ks / kTcAStages) & 1;
+        mbar_wait(full(s), ph);
+        mbar_wait(a_full(a), pa);
+        tc_fence_after();
+        const uint64_t bdesc = umma_desc_sw128(sB + s * L::kBBytes);
+#pragma unroll
+        for (int kk = 0; kk < kTcBK / 32; ++kk) {
+          // advance 32 K bytes inside the 128-byte swizzle atom: +2 in the (addr >> 4) field
+          tc_mma_i8(tmem, tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk), idesc, (ks | kk) != 0);
+        }
+        tc_commit(empty(s));
+        tc_commit(a_empty(a));
+      }
+      tc_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ converters
+    const int sub = warp - 4;            // TMEM sub-partition (lanes 32*sub ..)
+    const int r = sub * 32 + lane;       // row within the tile
+    const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
+    for (int ks = 0; ks < nk; ++ks) {
+      const int s = ks % STAGES;
+      const uint32_t ph = (ks / STAGES) & 1;
+      mbar_wait(full(s), ph);
+      uint4 v[WB];
+      const uint4* wsm = reinterpret_cast<const uint4*>(gbase + L::kWOff + s * L::kWBytes);
+#pragma unroll
+      for (int i = 0; i < WB; ++i) v[i] = wsm[i * kTcBM + r];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty(s));
+      uint32_t d[32];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t w[WB], o[8];
+#pragma unroll
+        for (int i = 0; i < WB; ++i) w[i] = j == 0 ? v[i].x : j == 1 ? v[i].y : j == 2 ? v[i].z : v[i].w;
+        rebuild8<WB>(w, o);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) d[8 * j + c] = o[c];
+      }
+      const int a = ks % kTcAStages;
+      const uint32_t pa = (ks / kTcAStages) & 1;
+      mbar_wait(a_empty(a), pa ^ 1);
+      tc_fence_after();
+      tmem_st32<32>(tmem + lane_off + kAcol0 + 32 * a, d);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full(a));
+    }
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int n = n0 + r;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t acc[32];
+      tmem_ld32(tmem + lane_off + c0, acc);
+      if (n < p.e.N) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int m = m0 + c0 + j;
+          if (m < p.e.M) epilogue_store(p.e, m, n, acc[j]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(ptr);
+  }
+  return fn;
+}
+
+int tc_stages(int wbits, int bn) {
+  const int stage = bn * kTcBK + wbits * kTcBM * 16;
+  const int budget = (bn <= 128 ? 110 : 220) * 1024;  // 2 CTAs per SM at BN = 128
+  int s = budget / stage;
+  if (s > 6) s = 6;
+  if (s < 2) s = 2;
+  return s;
+}
+
+size_t tc_workspace_bytes(int M, int k_words) { return (size_t)M * (size_t)k_words * 32u; }
+
+template <int WB, int BN, int ST>
+static cudaError_t launch_tc3(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, cudaStream_t stream) {
+  using L = TcSmem<WB, BN, ST>;
+  auto kern = gemm_tc_kernel<WB, BN, ST>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+  if (err != cudaSuccess) return err;
+  dim3 grid((p.e.N + kTcBM - 1) / kTcBM, (p.e.M + BN - 1) / BN);
+  kern<<<grid, 256, L::kTotal, stream>>>(tw, tb, p);
+  return cudaGetLastError();
+}
+
+template <int WB, int BN>
+static cudaError_t launch_tc2(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int stages,
+                              cudaStream_t stream) {
+  switch (stages) {
+    case 2: return launch_tc3<WB, BN, 2>(tw, tb, p, stream);
+    case 3: return launch_tc3<WB, BN, 3>(tw, tb, p, stream);
+    case 4: return launch_tc3<WB, BN, 4>(tw, tb, p, stream);
+    case 5: return launch_tc3<WB, BN, 5>(tw, tb, p, stream);
+    default: return launch_tc3<WB, BN, 6>(tw, tb, p, stream);
+  }
+}
+
+template <int WB>
+static cudaError_t launch_tc1(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int bn, int stages,
+                              cudaStream_t stream) {
+  if (bn == 256) return launch_tc2<WB, 256>(tw, tb, p, stages, stream);
+  return launch_tc2<WB, 128>(tw, tb, p, stages, stream);
+}
+
+cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int stages, void* workspace, cudaStream_t stream) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  // 1) token expand pre-pass into the workspace
+  {
+    const int64_t total = (int64_t)p.e.M * p.k_words;
+    const int blocks = (int)((total + 255) / 256);
+    expand_tokens_kernel<<<blocks, 256, 0, stream>>>(p.ap, p.a_pstride, p.e.M, p.k_words, p.abits,
+                                                     reinterpret_cast<uint8_t*>(workspace));
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
+  // 2) tensor maps
+  CUtensorMap tw, tb;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)p.k_words, (cuuint64_t)p.e.N, (cuuint64_t)wbits};
+    cuuint64_t strides[2] = {(cuuint64_t)p.k_words * 4, (cuuint64_t)p.w_pstride * 4};
+    cuuint32_t box[3] = {4, (cuuint32_t)kTcBM, (cuuint32_t)wbits};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(p.wp), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t kp = (cuuint64_t)p.k_words * 32;
+    cuuint64_t dims[2] = {kp, (cuuint64_t)p.e.M};
+    cuuint64_t strides[1] = {kp};
+    cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)bn};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, workspace, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  switch (wbits) {
+    case 1: return launch_tc1<1>(tw, tb, p, bn, stages, stream);
+    case 2: return launch_tc1<2>(tw, tb, p, bn, stages, stream);
+    case 3: return launch_tc1<3>(tw, tb, p, bn, stages, stream);
+    case 4: return launch_tc1<4>(tw, tb, p, bn, stages, stream);
+    case 5: return launch_tc1<5>(tw, tb, p, bn, stages, stream);
+    case 6: return launch_tc1<6>(tw, tb, p, bn, stages, stream);
+    case 7: return launch_tc1<7>(tw, tb, p, bn, stages, stream);
+    default: return launch_tc1<8>(tw, tb, p, bn, stages, stream);
+  }
+}
+
+}  // namespace apt

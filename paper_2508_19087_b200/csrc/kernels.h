@@ -32,3 +32,18 @@ cudaError_t launch_gemm_mma(const MmaArgs& p, int wbits, int bn, int split, cuda
 size_t mma_smem_bytes(int bn);
 
 }  // namespace apt
+
+namespace apt {
+struct TcArgs {
+  const uint32_t* wp;      // weight planes [wbits][N][k_words]
+  int64_t w_pstride;       // N * k_words
+  const uint32_t* ap;      // activation planes [abits][M][k_words]
+  int64_t a_pstride;       // M * k_words
+  int32_t k_words;
+  int32_t abits;
+  EpilogueArgs e;
+};
+cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int stages, void* workspace, cudaStream_t stream);
+int tc_stages(int wbits, int bn);
+size_t tc_workspace_bytes(int M, int k_words);
+}  // namespace apt
