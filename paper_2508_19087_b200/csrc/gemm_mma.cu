@@ -50,114 +50,129 @@ template <int WB, int NT>
 __global__ void __launch_bounds__(128) gemm_mma_kernel(MmaArgs p) {
   constexpr int BN = NT * 8;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint2* sB = reinterpret_cast<uint2*>(smem_raw);           // token digits, kKch words
-  int32_t* part = reinterpret_cast<int32_t*>(smem_raw);     // reused after the K loop: [BN][64]
+  uint2* sB = reinterpret_cast<uint2*>(smem_raw);                          // token digits, kKch words
+  int32_t* rbuf = reinterpret_cast<int32_t*>(smem_raw + (size_t)kKch * 32 * BN);  // [S][slots][64] partials
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int N = p.e.N, M = p.e.M;
+  const int S = gridDim.z;
+  const int slots = (BN + S - 1) / S;                      // tokens owned per rank in the reduction
   const int row0 = blockIdx.x * 64 + warp * 16 + g;        // rows row0 and row0 + 8
   const int tok0 = blockIdx.y * BN;
-  const uint32_t rank = (gridDim.z > 1) ? cluster_ctarank() : 0u;
+  const uint32_t rank = (S > 1) ? cluster_ctarank() : 0u;
+  // every CTA of the cluster must have started before anyone stores into its shared memory:
+  // arrive now, wait just before the reduction pushes (overlaps with the whole K loop)
+  if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const int kw_begin = (int)rank * p.kw_per_split;
   const int kw_end = min(p.k_words, kw_begin + p.kw_per_split);
+  const int n_it = kw_end > kw_begin ? (kw_end - kw_begin) >> 3 : 0;
 
   const bool ok0 = row0 < N, ok1 = row0 + 8 < N;
-  const uint32_t* w0 = p.wp + (int64_t)(ok0 ? row0 : 0) * p.k_words + 2 * t;
-  const uint32_t* w1 = p.wp + (int64_t)(ok1 ? row0 + 8 : 0) * p.k_words + 2 * t;
+  const uint32_t* w0 = p.wp + (int64_t)(ok0 ? row0 : 0) * p.k_words + 2 * t + kw_begin;
+  const uint32_t* w1 = p.wp + (int64_t)(ok1 ? row0 + 8 : 0) * p.k_words + 2 * t + kw_begin;
 
   int acc[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
 
-  for (int chunk = kw_begin; chunk < kw_end; chunk += kKch) {
-    const int nwc = min(kKch, kw_end - chunk);
-    __syncthreads();
-    // ---- token rebuild: planes -> u8 digits in the MMA K order, once per CTA chunk
-    for (int idx = threadIdx.x; idx < BN * nwc; idx += blockDim.x) {
-      const int n = idx / nwc, o = idx - n * nwc;
-      const int tok = tok0 + n;
-      uint32_t w[8];
+  // first iteration's weight words are requested before anything else (HBM latency is the bound)
+  uint2 cur0[WB], cur1[WB];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        w[i] = (i < p.abits && tok < M) ? __ldg(p.ap + (int64_t)i * p.a_pstride + (int64_t)tok * p.k_words + chunk + o) : 0u;
-      uint32_t d[8];
-      rebuild8_rt(w, p.abits, d);
-      const int it = o >> 3, r = o & 7, tt = r >> 1, gr = r & 1;
+  for (int i = 0; i < WB; ++i) {
+    cur0[i] = (n_it > 0 && ok0) ? __ldg(reinterpret_cast<const uint2*>(w0 + (int64_t)i * p.w_pstride)) : make_uint2(0, 0);
+    cur1[i] = (n_it > 0 && ok1) ? __ldg(reinterpret_cast<const uint2*>(w1 + (int64_t)i * p.w_pstride)) : make_uint2(0, 0);
+  }
+  constexpr int kItPerChunk = kKch / 8;
+  for (int gi = 0; gi < n_it; ++gi) {
+    const int it = gi % kItPerChunk;
+    if (it == 0) {
+      // ---- token rebuild: planes -> u8 digits in the MMA K order, once per CTA chunk
+      const int chunk = kw_begin + gi * 8;
+      const int nwc = min(kKch, kw_end - chunk);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < BN * nwc; idx += blockDim.x) {
+        const int n = idx / nwc, o = idx - n * nwc;
+        const int tok = tok0 + n;
+        uint32_t w[8];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) sB[sb_index(it, gr, s, n, tt, BN)] = make_uint2(d[2 * s], d[2 * s + 1]);
+        for (int i = 0; i < 8; ++i)
+          w[i] = (i < p.abits && tok < M)
+                     ? __ldg(p.ap + (int64_t)i * p.a_pstride + (int64_t)tok * p.k_words + chunk + o) : 0u;
+        uint32_t d[8];
+        rebuild8_rt(w, p.abits, d);
+        const int iq = o >> 3, r = o & 7, tt = r >> 1, gr = r & 1;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) sB[sb_index(iq, gr, s, n, tt, BN)] = make_uint2(d[2 * s], d[2 * s + 1]);
+      }
+      __syncthreads();
     }
-    __syncthreads();
-
-    // ---- main loop: 8 plane words (256 K elements) per iteration, next iteration prefetched
-    const int iters = nwc >> 3;
-    uint2 cur0[WB], cur1[WB];
+    // ---- prefetch the next 8 plane words of both rows, then rebuild + MMA on the current ones
+    uint2 nxt0[WB], nxt1[WB];
+    const bool more = gi + 1 < n_it;
 #pragma unroll
     for (int i = 0; i < WB; ++i) {
-      cur0[i] = ok0 ? __ldg(reinterpret_cast<const uint2*>(w0 + (int64_t)i * p.w_pstride + chunk)) : make_uint2(0, 0);
-      cur1[i] = ok1 ? __ldg(reinterpret_cast<const uint2*>(w1 + (int64_t)i * p.w_pstride + chunk)) : make_uint2(0, 0);
+      const int64_t off = (int64_t)i * p.w_pstride + (gi + 1) * 8;
+      nxt0[i] = (more && ok0) ? __ldg(reinterpret_cast<const uint2*>(w0 + off)) : make_uint2(0, 0);
+      nxt1[i] = (more && ok1) ? __ldg(reinterpret_cast<const uint2*>(w1 + off)) : make_uint2(0, 0);
     }
-    for (int it = 0; it < iters; ++it) {
-      uint2 nxt0[WB], nxt1[WB];
-      const bool more = it + 1 < iters;
+#pragma unroll
+    for (int gr = 0; gr < 2; ++gr) {
+      uint32_t wa[WB], wb[WB], ra[8], rb[8];
 #pragma unroll
       for (int i = 0; i < WB; ++i) {
-        const int64_t off = (int64_t)i * p.w_pstride + chunk + (it + 1) * 8;
-        nxt0[i] = (more && ok0) ? __ldg(reinterpret_cast<const uint2*>(w0 + off)) : make_uint2(0, 0);
-        nxt1[i] = (more && ok1) ? __ldg(reinterpret_cast<const uint2*>(w1 + off)) : make_uint2(0, 0);
+        wa[i] = gr ? cur0[i].y : cur0[i].x;
+        wb[i] = gr ? cur1[i].y : cur1[i].x;
       }
+      rebuild8<WB>(wa, ra);
+      rebuild8<WB>(wb, rb);
 #pragma unroll
-      for (int gr = 0; gr < 2; ++gr) {
-        uint32_t wa[WB], wb[WB], ra[8], rb[8];
+      for (int s = 0; s < 4; ++s) {
 #pragma unroll
-        for (int i = 0; i < WB; ++i) {
-          wa[i] = gr ? cur0[i].y : cur0[i].x;
-          wb[i] = gr ? cur1[i].y : cur1[i].x;
-        }
-        rebuild8<WB>(wa, ra);
-        rebuild8<WB>(wb, rb);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-#pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const uint2 b = sB[sb_index(it, gr, s, j * 8 + g, t, BN)];
-            mma_u8(acc[j], ra[2 * s], rb[2 * s], ra[2 * s + 1], rb[2 * s + 1], b.x, b.y);
-          }
+        for (int j = 0; j < NT; ++j) {
+          const uint2 b = sB[sb_index(it, gr, s, j * 8 + g, t, BN)];
+          mma_u8(acc[j], ra[2 * s], rb[2 * s], ra[2 * s + 1], rb[2 * s + 1], b.x, b.y);
         }
       }
-#pragma unroll
-      for (int i = 0; i < WB; ++i) { cur0[i] = nxt0[i]; cur1[i] = nxt1[i]; }
     }
+#pragma unroll
+    for (int i = 0; i < WB; ++i) { cur0[i] = nxt0[i]; cur1[i] = nxt1[i]; }
   }
 
-  // ---- partial tile -> shared memory, [token][64 rows]
-  __syncthreads();
+  // ---- split-K reduction: every partial is pushed (DSMEM store) to the rank that owns its token
+  //      (owner = token % S), one cluster barrier, then each rank sums its slice and stores it.
   const int lrow = warp * 16 + g;
+  const uint32_t rb_local = smem_u32(rbuf);
+  if (S > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    const int tk = j * 8 + 2 * t;
-    part[tk * 64 + lrow] = acc[j][0];
-    part[(tk + 1) * 64 + lrow] = acc[j][1];
-    part[tk * 64 + lrow + 8] = acc[j][2];
-    part[(tk + 1) * 64 + lrow + 8] = acc[j][3];
-  }
-  const int S = gridDim.z;
-  if (S > 1) cluster_sync_all(); else __syncthreads();
-  if (rank == 0) {
-    for (int idx = threadIdx.x; idx < BN * 64; idx += blockDim.x) {
-      int tk, lr;
-      if (p.e.layout == 0) { tk = idx >> 6; lr = idx & 63; }   // consecutive rows n -> coalesced
-      else { tk = idx % BN; lr = idx / BN; }                  // consecutive tokens m -> coalesced
-      const int m = tok0 + tk, n = blockIdx.x * 64 + lr;
-      uint32_t U = (uint32_t)part[tk * 64 + lr];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int tk = j * 8 + 2 * t + (h & 1);
+      const int lr = lrow + (h >> 1) * 8;
+      const int owner = tk % S, slot = tk / S;
+      const uint32_t off = (uint32_t)((((int)rank * slots + slot) * 64 + lr) * 4);
       if (S > 1) {
-        const uint32_t a = smem_u32(part + tk * 64 + lr);
-        for (int q = 1; q < S; ++q) U += ld_dsmem_u32(a, (uint32_t)q);
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(rb_local + off), "r"(owner));
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(remote), "r"(acc[j][h]) : "memory");
+      } else {
+        rbuf[off / 4] = acc[j][h];
       }
-      if (m < M && n < N) epilogue_store(p.e, m, n, U);
     }
   }
-  if (S > 1) cluster_sync_all();  // keep every rank's shared memory alive until rank 0 has read it
+  if (S > 1) cluster_sync_all(); else __syncthreads();
+  const int mine = (BN - (int)rank + S - 1) / S;  // tokens tk = rank + S*slot < BN
+  for (int idx = threadIdx.x; idx < mine * 64; idx += blockDim.x) {
+    int slot, lr;
+    if (p.e.layout == 0) { slot = idx >> 6; lr = idx & 63; }   // consecutive rows n -> coalesced
+    else { slot = idx % mine; lr = idx / mine; }
+    const int tk = (int)rank + S * slot;
+    const int m = tok0 + tk, n = blockIdx.x * 64 + lr;
+    uint32_t U = 0;
+    for (int src = 0; src < S; ++src) U += (uint32_t)rbuf[(src * slots + slot) * 64 + lr];
+    if (m < M && n < N) epilogue_store(p.e, m, n, U);
+  }
 }
 
 template <int WB, int NT>
@@ -190,15 +205,15 @@ static cudaError_t launch_wb(const MmaArgs& p, int nt, int split, size_t smem, c
   }
 }
 
-size_t mma_smem_bytes(int bn) {
-  const size_t sb = (size_t)kKch * 8 * 4 * bn;  // 32 bytes per word per token
-  const size_t pt = (size_t)bn * 64 * 4;
-  return sb > pt ? sb : pt;
+size_t mma_smem_bytes(int bn, int split) {
+  const size_t sb = (size_t)kKch * 8 * 4 * bn;                        // 32 bytes per word per token
+  const size_t rb = (size_t)split * ((bn + split - 1) / split) * 64 * 4;  // reduction receive buffer
+  return sb + rb;
 }
 
 cudaError_t launch_gemm_mma(const MmaArgs& p, int wbits, int bn, int split, cudaStream_t stream) {
   const int nt = bn / 8;
-  const size_t smem = mma_smem_bytes(bn);
+  const size_t smem = mma_smem_bytes(bn, split);
   switch (wbits) {
     case 1: return launch_wb<1>(p, nt, split, smem, stream);
     case 2: return launch_wb<2>(p, nt, split, smem, stream);

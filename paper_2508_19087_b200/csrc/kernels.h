@@ -29,7 +29,7 @@ struct MmaArgs {
   EpilogueArgs e;
 };
 cudaError_t launch_gemm_mma(const MmaArgs& p, int wbits, int bn, int split, cudaStream_t stream);
-size_t mma_smem_bytes(int bn);
+size_t mma_smem_bytes(int bn, int split);
 
 }  // namespace apt
 

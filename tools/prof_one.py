@@ -1,0 +1,37 @@
+"""Run one APT GEMM configuration a few times (for ncu captures).
+
+  python tools/prof_one.py M N K wbits abits [reps] [bn]
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2508_19087_b200 as P  # noqa: E402
+
+
+def main():
+    m, n, k, wb, ab = (int(v) for v in sys.argv[1:6])
+    reps = int(sys.argv[6]) if len(sys.argv) > 6 else 3
+    bn = int(sys.argv[7]) if len(sys.argv) > 7 else 0
+    dev = torch.device("cuda")
+    W = P.pack(torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev), wb)
+    a = torch.randint(-(1 << (ab - 1)), 1 << (ab - 1), (m, k), dtype=torch.int8, device=dev)
+    A = P.pack(a, ab)
+    ws = torch.rand(n, device=dev)
+    cfg = P.select_config(m, n, k, wb, ab)
+    if bn and cfg["kernel"] == 2:
+        cfg["bn"] = bn
+        stage = bn * 128 + wb * 128 * 16
+        cfg["stages"] = max(2, min(6, ((110 if bn <= 128 else 220) * 1024) // stage))
+    out = torch.empty((m, n), dtype=torch.float16, device=dev)
+    for _ in range(reps):
+        P.pack(a, ab, out=A)
+        P.gemm(W, A, out_kind="f16", w_scale=ws, out=out, config=cfg)
+    torch.cuda.synchronize()
+    print("cfg", cfg)
+
+
+if __name__ == "__main__":
+    main()
