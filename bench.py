@@ -235,7 +235,7 @@ def main():
             W_scale[(wb, n, k)] = scales(shard[n], -10, -6)
     A_codes = {(m, ab, k): codes(m, k, ab) for m in MS for ab in {a for _, a in PRECISIONS} for k in {k for _, k in SHAPES}}
     A_scale = {m: scales(m, -6, -2) for m in MS}
-    A_buf = {key: P.alloc_packed(key[0], key[2], key[1], dev) for key in A_codes}
+    A_buf = {key: P.alloc_packed(key[0], key[2], key[1], dev, digits=True) for key in A_codes}
     layout = "row" if world == 1 else "col"
     outs = [torch.empty((m, shard[n]) if world == 1 else (shard[n], m), dtype=torch.float16, device=dev)
             for (m, wb, ab, n, k) in CASES]
@@ -384,7 +384,7 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
             lo, hi = -(1 << (ab - 1)), (1 << (ab - 1))
             h_a[(m, ab, k)] = torch.randint(lo, hi, (m, k), dtype=torch.int8).pin_memory()
     d_a = {key: torch.empty(t.shape, dtype=torch.int8, device=dev) for key, t in h_a.items()}
-    bufs = {key: P.alloc_packed(key[0], key[2], key[1], dev) for key in h_a}
+    bufs = {key: P.alloc_packed(key[0], key[2], key[1], dev, digits=True) for key in h_a}
     d_out = [torch.empty((m, shard[n]) if world == 1 else (shard[n], m), dtype=torch.float16, device=dev)
              for (m, wb, ab, n, k) in CASES]
     h_out = [torch.empty(o.shape, dtype=torch.float16).pin_memory() for o in d_out]

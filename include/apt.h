@@ -70,7 +70,13 @@ typedef enum {
  *             Must be 16-byte aligned.
  *   row_sum : int32 [rows], sum_{c<k} of the signed codes of the row (used by the rank-1 terms of
  *             the epilogue; SURVEY §8c identities I2/I3).
- *   rows, k : logical shape; k_words = Kpad / 32; bits = n in [1, 8].                              */
+ *   rows, k : logical shape; k_words = Kpad / 32; bits = n in [1, 8].
+ *   digits  : OPTIONAL (may be NULL) uint8 [rows][Kpad], 16-byte aligned: the same codes as unsigned
+ *             digits u in the GEMM kernels' internal K order (within every 32-element word the
+ *             element order of the on-chip operand rebuild; word order unchanged).  When non-NULL,
+ *             apt_pack_bipolar fills it in the same pass, and apt_gemm reads the ACTIVATION operand
+ *             from it instead of rebuilding the activation planes (the weight operand is always read
+ *             as planes).  Intended for the small per-call activation matrix.                       */
 typedef struct {
   int32_t rows;
   int32_t k;
@@ -78,6 +84,7 @@ typedef struct {
   int32_t bits;
   uint32_t* planes;
   int32_t* row_sum;
+  uint8_t* digits;
 } apt_packed;
 
 /* Host.  Bytes of the `planes` buffer for a rows x k matrix of n-bit codes:
@@ -134,9 +141,11 @@ typedef enum {
  *   bk       : K elements per pipeline step
  *   stages   : pipeline depth (TC kernel)
  *   split_k  : K splits (MMA_SPLITK kernel: the cluster size, 1..8)
- *   cta_pair : 1 = cta_group::2 pairs (TC kernel), 0 = single CTA                                   */
+ *   cta_pair : 1 = cta_group::2 pairs (TC kernel), 0 = single CTA (this build: 0)
+ *   cluster_n: TC kernel: CTAs along N (weight tiles) sharing one token tile; the token tile is loaded
+ *              once per cluster with TMA multicast (1, 2 or 4)                                          */
 typedef struct {
-  int32_t kernel, w_digit, a_digit, bm, bn, bk, stages, split_k, cta_pair;
+  int32_t kernel, w_digit, a_digit, bm, bn, bk, stages, split_k, cta_pair, cluster_n;
 } apt_config;
 
 /* Host, pure and deterministic (replaces the paper's lookup table + search, §5.2).

@@ -7,7 +7,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libapt.so")
+# APT_LIB_VARIANT selects an in-tree experiment build (tools/ only); default is libapt.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("APT_LIB_VARIANT", "libapt.so"))
 
 APT_OK, APT_ERR_INVALID_ARGUMENT, APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ERR_CUDA = range(5)
 APT_ENC_SIGNED, APT_ENC_BIPOLAR = 0, 1
@@ -21,7 +22,8 @@ EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_select_config", "
 
 class AptPacked(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int32), ("k", ctypes.c_int32), ("k_words", ctypes.c_int32),
-                ("bits", ctypes.c_int32), ("planes", ctypes.c_void_p), ("row_sum", ctypes.c_void_p)]
+                ("bits", ctypes.c_int32), ("planes", ctypes.c_void_p), ("row_sum", ctypes.c_void_p),
+                ("digits", ctypes.c_void_p)]
 
 
 class AptScales(ctypes.Structure):
@@ -30,7 +32,8 @@ class AptScales(ctypes.Structure):
 
 class AptConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
-                ("kernel", "w_digit", "a_digit", "bm", "bn", "bk", "stages", "split_k", "cta_pair")]
+                ("kernel", "w_digit", "a_digit", "bm", "bn", "bk", "stages", "split_k", "cta_pair",
+                 "cluster_n")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

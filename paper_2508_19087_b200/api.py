@@ -37,12 +37,14 @@ def _require_cuda(t: torch.Tensor, name: str):
 @dataclass
 class Packed:
     """The packed "unified matrix": planes [bits][rows][k_words] uint32 (stored as int32
-    tensor), row_sum [rows] int32."""
+    tensor), row_sum [rows] int32, and optionally the kernel-order u8 digit view [rows][Kpad]
+    (written by the pack kernel in the same pass; used for activations)."""
     planes: torch.Tensor
     row_sum: torch.Tensor
     rows: int
     k: int
     bits: int
+    digits: torch.Tensor | None = None
 
     @property
     def k_words(self) -> int:
@@ -50,30 +52,34 @@ class Packed:
 
     def struct(self) -> L.AptPacked:
         return L.AptPacked(self.rows, self.k, self.k_words, self.bits, self.planes.data_ptr(),
-                           self.row_sum.data_ptr())
+                           self.row_sum.data_ptr(), self.digits.data_ptr() if self.digits is not None else None)
 
     def narrow_rows(self, start: int, length: int) -> "Packed":
         """Rows [start, start+length) as a new packed matrix (copies the plane slices)."""
         planes = self.planes[:, start:start + length].contiguous()
-        return Packed(planes, self.row_sum[start:start + length].contiguous(), length, self.k, self.bits)
+        digits = self.digits[start:start + length].contiguous() if self.digits is not None else None
+        return Packed(planes, self.row_sum[start:start + length].contiguous(), length, self.k, self.bits, digits)
 
 
-def alloc_packed(rows: int, k: int, bits: int, device) -> Packed:
+def alloc_packed(rows: int, k: int, bits: int, device, digits: bool = False) -> Packed:
+    """Buffers for a packed operand; ``digits=True`` also allocates the u8 digit view (activations)."""
     kw = kpad(k) // 32
     planes = torch.empty((bits, rows, kw), dtype=torch.int32, device=device)
     row_sum = torch.empty((rows,), dtype=torch.int32, device=device)
-    return Packed(planes, row_sum, rows, k, bits)
+    dig = torch.empty((rows, kw * 32), dtype=torch.uint8, device=device) if digits else None
+    return Packed(planes, row_sum, rows, k, bits, dig)
 
 
 def pack(codes: torch.Tensor, bits: int, encoding: str = "signed", out: Packed | None = None,
-         range_error: torch.Tensor | None = None, stream=None) -> Packed:
-    """apt_pack_bipolar: int8 codes [rows, k] (row stride ``codes.stride(0)``) -> Packed."""
+         range_error: torch.Tensor | None = None, stream=None, digits: bool = False) -> Packed:
+    """apt_pack_bipolar: int8 codes [rows, k] (row stride ``codes.stride(0)``) -> Packed.
+    ``digits=True`` (activations) also emits the kernel-order u8 digit view in the same pass."""
     _require_cuda(codes, "codes")
     if codes.dtype != torch.int8 or codes.dim() != 2 or codes.stride(1) != 1:
         raise ValueError("codes must be a 2-D int8 tensor with unit stride along K")
     rows, k = codes.shape
     if out is None:
-        out = alloc_packed(rows, k, bits, codes.device)
+        out = alloc_packed(rows, k, bits, codes.device, digits=digits)
     st = out.struct()
     rc = L.lib().apt_pack_bipolar(codes.data_ptr(), rows, k, codes.stride(0), bits, _ENCODINGS[encoding],
                                   ctypes.byref(st), range_error.data_ptr() if range_error is not None else None,
@@ -131,14 +137,13 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
         sc = L.AptScales(w_scale.data_ptr() if w_scale is not None else None,
                          a_scale.data_ptr() if a_scale is not None else None)
     c = _config_struct(config)
-    if c is None:
-        ws_need = 0
-    else:
-        ws_need = int(L.lib().apt_gemm_workspace_bytes(ctypes.byref(c), M, N, K))
-    if config is None:
-        sel = L.AptConfig()
-        L.check("apt_select_config", L.lib().apt_select_config(M, N, K, W.bits, A.bits, ctypes.byref(sel)))
-        ws_need = int(L.lib().apt_gemm_workspace_bytes(ctypes.byref(sel), M, N, K))
+    ws_need = 0
+    if A.digits is None:  # the activation digit view is expanded into the workspace
+        cc = c
+        if cc is None:
+            cc = L.AptConfig()
+            L.check("apt_select_config", L.lib().apt_select_config(M, N, K, W.bits, A.bits, ctypes.byref(cc)))
+        ws_need = int(L.lib().apt_gemm_workspace_bytes(ctypes.byref(cc), M, N, K))
     if ws_need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < ws_need):
         workspace = torch.empty((ws_need,), dtype=torch.uint8, device=W.planes.device)
     ws_ptr = workspace.data_ptr() if workspace is not None else None

@@ -34,16 +34,18 @@ apt_status validate_packed(const apt_packed* P, int32_t rows, int32_t k, int32_t
 apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits) {
   const int kw = (int)(kpad_of(K) / 32);
   if (c->w_digit != wbits || c->a_digit != abits) return APT_ERR_UNSUPPORTED;  // full-width digits only
+  (void)kw;
   if (c->kernel == APT_KERNEL_MMA_SPLITK) {
-    if (c->bm != 64 || c->bk != 256) return APT_ERR_UNSUPPORTED;
-    if (c->bn != 8 && c->bn != 16 && c->bn != 32 && c->bn != 64) return APT_ERR_UNSUPPORTED;
-    if (c->split_k < 1 || c->split_k > 8 || c->split_k > kw / 8) return APT_ERR_UNSUPPORTED;
-    if (c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
+    if (c->bm != 16 || c->bk != 256) return APT_ERR_UNSUPPORTED;
+    if (c->bn != 8 && c->bn != 16) return APT_ERR_UNSUPPORTED;
+    if (c->split_k < 1 || c->split_k > 8) return APT_ERR_UNSUPPORTED;
+    if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
     return APT_OK;
   }
   if (c->kernel == APT_KERNEL_TC) {
     if (c->bm != 128 || c->bk != 128 || (c->bn != 128 && c->bn != 256)) return APT_ERR_UNSUPPORTED;
-    if (c->stages < 2 || c->stages > 6 || c->split_k != 1 || c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
+    if (c->stages != apt::tc_stages(wbits, c->bn) || c->split_k != 1 || c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
+    if (c->cluster_n != 1 && c->cluster_n != 2 && c->cluster_n != 4) return APT_ERR_UNSUPPORTED;
     return APT_OK;
   }
   return APT_ERR_UNSUPPORTED;
@@ -93,6 +95,8 @@ apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k, int64_
   p.plane_stride = (int64_t)rows * out->k_words;
   p.row_sum = out->row_sum;
   p.range_error = range_error;
+  p.digits = out->digits;
+  if (out->digits && !aligned16(out->digits)) return APT_ERR_INVALID_ARGUMENT;
   cudaError_t err = apt::launch_pack(p, bits, reinterpret_cast<cudaStream_t>(stream));
   return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
 }
@@ -114,30 +118,27 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
     out->stages = apt::tc_stages(wbits, out->bn);
     out->split_k = 1;
     out->cta_pair = 0;
+    out->cluster_n = ceil_div(N, 128) >= 4 ? 4 : ceil_div(N, 128) >= 2 ? 2 : 1;
     return APT_OK;
   }
+  // decode: 16 weight rows per CTA, K split over 8 warps, tokens in tiles of 8 or 16
   out->kernel = APT_KERNEL_MMA_SPLITK;
-  out->bm = 64;
+  out->cluster_n = 1;
+  out->bm = 16;
   out->bk = 256;
   out->stages = 2;
   out->cta_pair = 0;
-  out->bn = M <= 8 ? 8 : M <= 16 ? 16 : M <= 32 ? 32 : 64;
-  // split-K so that the grid holds >= 4 CTAs per SM (HBM latency hiding for decode shapes),
-  // each split covering at least one 256-element iteration; cluster size <= 8 (portable)
-  const int64_t tiles = (int64_t)ceil_div(N, 64) * ceil_div(M, out->bn);
-  int split = (int)((4 * kNumSMs + tiles - 1) / tiles);
-  if (split > 8) split = 8;
-  if (split > kw / 8) split = kw / 8;
-  if (split < 1) split = 1;
-  out->split_k = split;
+  out->bn = M <= 8 ? 8 : 16;
+  out->split_k = 8;
+  (void)kw;
   return APT_OK;
 }
 
 size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
+  // activation digit view for activations packed without one (apt_packed.digits == NULL)
   (void)N;
   if (!cfg || M <= 0 || K <= 0) return 0;
-  if (cfg->kernel == APT_KERNEL_TC) return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
-  return 0;
+  return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
 }
 
 apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, const apt_packed* W,
@@ -165,8 +166,9 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   }
   st = validate_config(&c, M, N, K, wbits, abits);
   if (st != APT_OK) return st;
-  const size_t need = apt_gemm_workspace_bytes(&c, M, N, K);
-  if (need > 0 && (!workspace || ws_bytes < need)) return APT_ERR_WORKSPACE;
+  const size_t need = A->digits ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
+  if (need > 0 && (!workspace || ws_bytes < need || !aligned16(workspace))) return APT_ERR_WORKSPACE;
+  if (A->digits && !aligned16(A->digits)) return APT_ERR_INVALID_ARGUMENT;
 
   apt::EpilogueArgs e;
   e.w_rowsum = W->row_sum;
@@ -184,33 +186,32 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   e.h_w = 1 << (wbits - 1);
   e.h_a = 1 << (abits - 1);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-
+  // the activation operand as kernel-order u8 digits: the packed view, or expanded now
+  const uint8_t* adig = A->digits;
+  if (!adig) {
+    cudaError_t err = apt::launch_expand_tokens(A->planes, (int64_t)M * A->k_words, M, A->k_words, abits,
+                                                reinterpret_cast<uint8_t*>(workspace), s);
+    if (err != cudaSuccess) return APT_ERR_CUDA;
+    adig = reinterpret_cast<const uint8_t*>(workspace);
+  }
   if (c.kernel == APT_KERNEL_MMA_SPLITK) {
     apt::MmaArgs p;
     p.wp = W->planes;
     p.w_pstride = (int64_t)N * W->k_words;
-    p.ap = A->planes;
-    p.a_pstride = (int64_t)M * A->k_words;
+    p.adig = adig;
     p.k_words = W->k_words;
-    p.abits = abits;
-    const int per = ceil_div(W->k_words, c.split_k);
-    p.kw_per_split = ((per + 7) / 8) * 8;
     p.e = e;
-    const int split = ceil_div(W->k_words, p.kw_per_split);
-    cudaError_t err = apt::launch_gemm_mma(p, wbits, c.bn, split, s);
+    cudaError_t err = apt::launch_gemm_mma(p, wbits, c.bn, c.split_k, s);
     return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   if (c.kernel == APT_KERNEL_TC) {
-    if (!aligned16(workspace)) return APT_ERR_WORKSPACE;
     apt::TcArgs p;
     p.wp = W->planes;
     p.w_pstride = (int64_t)N * W->k_words;
-    p.ap = A->planes;
-    p.a_pstride = (int64_t)M * A->k_words;
+    p.adig = adig;
     p.k_words = W->k_words;
-    p.abits = abits;
     p.e = e;
-    cudaError_t err = apt::launch_gemm_tc(p, wbits, c.bn, c.stages, workspace, s);
+    cudaError_t err = apt::launch_gemm_tc(p, wbits, c.bn, c.cluster_n, s);
     return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   return APT_ERR_UNSUPPORTED;

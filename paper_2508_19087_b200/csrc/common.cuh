@@ -101,9 +101,10 @@ struct EpilogueArgs {
   int32_t h_w, h_a;         // 2^(wbits-1), 2^(abits-1)
 };
 
-__device__ __forceinline__ void epilogue_store(const EpilogueArgs& e, int m, int n, uint32_t U) {
-  const uint32_t ra = (uint32_t)__ldg(e.a_rowsum + m);
-  const uint32_t rw = (uint32_t)__ldg(e.w_rowsum + n);
+// Epilogue with the rank-1 / scale operands already in registers.
+__device__ __forceinline__ void epilogue_store_v(const EpilogueArgs& e, int m, int n, uint32_t U, int32_t ra_,
+                                                 int32_t rw_, float wsc, float asc) {
+  const uint32_t ra = (uint32_t)ra_, rw = (uint32_t)rw_;
   const uint32_t y = U - (uint32_t)e.h_w * ra - (uint32_t)e.h_a * rw -
                      (uint32_t)e.kpad * (uint32_t)e.h_a * (uint32_t)e.h_w;
   const int64_t off = e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m;
@@ -113,12 +114,16 @@ __device__ __forceinline__ void epilogue_store(const EpilogueArgs& e, int m, int
     const uint32_t yb = 4u * y + 2u * ra + 2u * rw + (uint32_t)e.K;
     reinterpret_cast<int32_t*>(e.out)[off] = (int32_t)yb;
   } else {
-    float v = (float)(int32_t)y * __ldg(e.w_scale + n);
-    if (e.a_scale) v = v * __ldg(e.a_scale + m);
+    const float v = ((float)(int32_t)y * wsc) * asc;
     unsigned short h;
     asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(v));
     reinterpret_cast<unsigned short*>(e.out)[off] = h;
   }
+}
+
+__device__ __forceinline__ void epilogue_store(const EpilogueArgs& e, int m, int n, uint32_t U) {
+  epilogue_store_v(e, m, n, U, __ldg(e.a_rowsum + m), __ldg(e.w_rowsum + n),
+                   e.kind == 2 ? __ldg(e.w_scale + n) : 0.f, (e.kind == 2 && e.a_scale) ? __ldg(e.a_scale + m) : 1.f);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -33,6 +33,13 @@ namespace apt {
 constexpr int kTcBM = 128;       // weight rows per tile (MMA M)
 constexpr int kTcBK = 128;       // K elements per pipeline step
 constexpr int kTcAStages = 4;    // TMEM A ring depth (32 columns each)
+#ifdef APT_TC_TRACE
+// per-stage clock64 timeline of CTA (APT_TC_TRACE_CTA, 0) for profiling builds only
+__device__ long long g_tc_trace[8][512];
+#define TRACE(slot, ks) do { if (blockIdx.x == APT_TC_TRACE_CTA && blockIdx.y == 0 && (ks) < 512) g_tc_trace[slot][(ks)] = clock64(); } while (0)
+#else
+#define TRACE(slot, ks) do { } while (0)
+#endif
 
 // ------------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -117,7 +124,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 // ------------------------------------------------------------------------------------ pre-pass
-// Activation planes [abits][M][k_words] -> u8 digits [M][Kpad] in rebuild8() order.
+// Activation planes [abits][M][k_words] -> u8 digits [M][Kpad] in rebuild8() order (used when the
+// packed activation carries no digit view).
 __global__ void __launch_bounds__(256) expand_tokens_kernel(const uint32_t* __restrict__ ap, int64_t a_pstride,
                                                             int32_t M, int32_t k_words, int32_t abits,
                                                             uint8_t* __restrict__ ws) {
@@ -133,6 +141,13 @@ __global__ void __launch_bounds__(256) expand_tokens_kernel(const uint32_t* __re
   dst[1] = make_uint4(d[4], d[5], d[6], d[7]);
 }
 
+cudaError_t launch_expand_tokens(const uint32_t* ap, int64_t a_pstride, int M, int k_words, int abits, uint8_t* out,
+                                 cudaStream_t stream) {
+  const int64_t total = (int64_t)M * k_words;
+  expand_tokens_kernel<<<(int)((total + 255) / 256), 256, 0, stream>>>(ap, a_pstride, M, k_words, abits, out);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------------ main kernel
 template <int WB, int BN, int STAGES>
 struct TcSmem {
@@ -140,12 +155,30 @@ struct TcSmem {
   static constexpr int kWBytes = WB * kTcBM * 16;       // weight planes per stage (4 words per row per plane)
   static constexpr int kBOff = 0;
   static constexpr int kWOff = STAGES * kBBytes;
-  static constexpr int kBarOff = kWOff + STAGES * kWBytes;
+  static constexpr int kEpOff = kWOff + STAGES * kWBytes;  // rw[128] ws[128] ra[BN] as[BN]
+  static constexpr int kBarOff = kEpOff + (2 * kTcBM + 2 * BN) * 4;
   static constexpr int kNumBars = 2 * STAGES + 2 * kTcAStages + 1;
   static constexpr int kTotal = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
 };
 
-template <int WB, int BN, int STAGES>
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
+
+// CN = CTAs of a cluster along the weight-row dimension sharing one token tile: each loads BN/CN
+// token rows and multicasts them to all CN, so the token tile crosses L2 -> SM once per cluster.
+template <int WB, int BN, int STAGES, int CN>
 __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w,
                                                          const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
   using L = TcSmem<WB, BN, STAGES>;
@@ -156,6 +189,10 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
   const uint32_t sB = base + L::kBOff;
   const uint32_t sW = base + L::kWOff;
   const uint32_t bars = base + L::kBarOff;
+  int32_t* ep_rw = reinterpret_cast<int32_t*>(gbase + L::kEpOff);
+  float* ep_ws = reinterpret_cast<float*>(ep_rw + kTcBM);
+  int32_t* ep_ra = reinterpret_cast<int32_t*>(ep_ws + kTcBM);
+  float* ep_as = reinterpret_cast<float*>(ep_ra + BN);
   auto full = [&](int s) { return bars + 8u * s; };
   auto empty = [&](int s) { return bars + 8u * (STAGES + s); };
   auto a_full = [&](int a) { return bars + 8u * (2 * STAGES + a); };
@@ -164,16 +201,20 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::kBarOff + L::kNumBars * 8);
   constexpr uint32_t kTmemCols = (BN + 32 * kTcAStages) <= 256 ? 256 : 512;
   constexpr uint32_t kAcol0 = BN;  // A ring after the accumulator columns
+  constexpr int kRowsPerCta = BN / CN;
+  constexpr uint16_t kMask = (uint16_t)((1u << CN) - 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kTcBM;   // weight rows
   const int m0 = blockIdx.y * BN;      // tokens
   const int nk = p.k_words / 4;        // 128-element K steps
+  const uint32_t crank = CN > 1 ? cluster_ctarank() : 0u;
+  if (threadIdx.x == 0) TRACE(6, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(empty(s), 1 + 4);
+      mbar_init(empty(s), CN + 4);   // every CTA's MMA commit (multicast) + the 4 local converter warps
     }
     for (int a = 0; a < kTcAStages; ++a) {
       mbar_init(a_full(a), 4);
@@ -181,7 +222,6 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
     }
     mbar_init(acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_w) : "memory");
@@ -194,9 +234,10 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CN > 1) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+  if (threadIdx.x == 0) TRACE(6, 1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -206,8 +247,13 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
         const int s = ks % STAGES;
         const uint32_t ph = (ks / STAGES) & 1;
         mbar_wait(empty(s), ph ^ 1);
+        TRACE(0, ks);
         mbar_expect_tx(full(s), kTx);
-        tma_load_2d(sB + s * L::kBBytes, &tm_b, full(s), ks * kTcBK, m0);
+        const uint32_t dstB = sB + s * L::kBBytes + crank * kRowsPerCta * kTcBK;
+        if (CN > 1)
+          tma_load_2d_mc(dstB, &tm_b, full(s), ks * kTcBK, m0 + (int)crank * kRowsPerCta, kMask);
+        else
+          tma_load_2d(dstB, &tm_b, full(s), ks * kTcBK, m0);
         tma_load_3d(sW + s * L::kWBytes, &tm_w, full(s), ks * 4, n0, 0);
       }
     }
@@ -223,7 +269,9 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
         const int a = ks % kTcAStages;
         const uint32_t pa = (ks / kTcAStages) & 1;
         mbar_wait(full(s), ph);
+        TRACE(1, ks);
         mbar_wait(a_full(a), pa);
+        TRACE(2, ks);
         tc_fence_after();
         const uint64_t bdesc = umma_desc_sw128(sB + s * L::kBBytes);
 #pragma unroll
@@ -231,13 +279,27 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
           // advance 32 K bytes inside the 128-byte swizzle atom: +2 in the (addr >> 4) field
           tc_mma_i8(tmem, tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk), idesc, (ks | kk) != 0);
         }
-        tc_commit(empty(s));
+        if (CN > 1) tc_commit_mc(empty(s), kMask); else tc_commit(empty(s));
         tc_commit(a_empty(a));
       }
       tc_commit(acc_full);
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ converters
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ epilogue operands (warps 2, 3)
+    for (int i = threadIdx.x - 64; i < kTcBM + BN; i += 64) {
+      if (i < kTcBM) {
+        const int n = min(n0 + i, p.e.N - 1);
+        ep_rw[i] = __ldg(p.e.w_rowsum + n);
+        ep_ws[i] = p.e.kind == 2 ? __ldg(p.e.w_scale + n) : 0.f;
+      } else {
+        const int m = min(m0 + i - kTcBM, p.e.M - 1);
+        ep_ra[i - kTcBM] = __ldg(p.e.a_rowsum + m);
+        ep_as[i - kTcBM] = (p.e.kind == 2 && p.e.a_scale) ? __ldg(p.e.a_scale + m) : 1.f;
+      }
+    }
+    asm volatile("bar.arrive 1, 192;" ::: "memory");
+  } else {
+    // ------------------------------------------------------------ converters (warps 4..7)
     const int sub = warp - 4;            // TMEM sub-partition (lanes 32*sub ..)
     const int r = sub * 32 + lane;       // row within the tile
     const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
@@ -245,6 +307,7 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
       const int s = ks % STAGES;
       const uint32_t ph = (ks / STAGES) & 1;
       mbar_wait(full(s), ph);
+      if (lane == 0 && sub == 0) TRACE(3, ks);
       uint4 v[WB];
       const uint4* wsm = reinterpret_cast<const uint4*>(gbase + L::kWOff + s * L::kWBytes);
 #pragma unroll
@@ -270,11 +333,16 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full(a));
+      if (lane == 0 && sub == 0) TRACE(4, ks);
     }
     // ------------------------------------------------------------ epilogue
+    asm volatile("bar.sync 1, 192;" ::: "memory");   // epilogue operands are in shared memory
     mbar_wait(acc_full, 0);
+    if (lane == 0 && sub == 0) TRACE(5, 0);
     tc_fence_after();
     const int n = n0 + r;
+    const int32_t rw = ep_rw[r];
+    const float wsc = ep_ws[r];
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       uint32_t acc[32];
@@ -283,13 +351,16 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int m = m0 + c0 + j;
-          if (m < p.e.M) epilogue_store(p.e, m, n, acc[j]);
+          if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[j], ep_ra[c0 + j], rw, wsc, ep_as[c0 + j]);
         }
       }
     }
   }
+  if (warp == 4 && lane == 0) TRACE(5, 1);
+  if (threadIdx.x == 0) TRACE(5, 2);
   tc_fence_before();
-  __syncthreads();
+  // no CTA may leave while cluster peers can still multicast into it or arrive on its barriers
+  if (CN > 1) cluster_sync_all(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
@@ -313,60 +384,67 @@ static PFN_encodeTiled_t get_encode() {
   return fn;
 }
 
-int tc_stages(int wbits, int bn) {
-  const int stage = bn * kTcBK + wbits * kTcBM * 16;
-  const int budget = (bn <= 128 ? 110 : 220) * 1024;  // 2 CTAs per SM at BN = 128
-  int s = budget / stage;
-  if (s > 6) s = 6;
-  if (s < 2) s = 2;
-  return s;
+__host__ __device__ constexpr int tc_stages_ct(int wbits, int bn) {
+  // as deep as shared memory allows: ~108 KB per CTA at BN = 128 (two CTAs per SM), ~216 KB at 256
+  return ((bn <= 128 ? 108 : 216) * 1024) / (bn * kTcBK + wbits * kTcBM * 16) > 6
+             ? 6
+             : ((bn <= 128 ? 108 : 216) * 1024) / (bn * kTcBK + wbits * kTcBM * 16) < 2
+                   ? 2
+                   : ((bn <= 128 ? 108 : 216) * 1024) / (bn * kTcBK + wbits * kTcBM * 16);
 }
+
+int tc_stages(int wbits, int bn) { return tc_stages_ct(wbits, bn); }
 
 size_t tc_workspace_bytes(int M, int k_words) { return (size_t)M * (size_t)k_words * 32u; }
 
-template <int WB, int BN, int ST>
-static cudaError_t launch_tc3(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, cudaStream_t stream) {
+template <int WB, int BN, int ST, int CN>
+static cudaError_t launch_tc4(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, cudaStream_t stream) {
   using L = TcSmem<WB, BN, ST>;
-  auto kern = gemm_tc_kernel<WB, BN, ST>;
+  auto kern = gemm_tc_kernel<WB, BN, ST, CN>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
   if (err != cudaSuccess) return err;
-  dim3 grid((p.e.N + kTcBM - 1) / kTcBM, (p.e.M + BN - 1) / BN);
-  kern<<<grid, 256, L::kTotal, stream>>>(tw, tb, p);
-  return cudaGetLastError();
+  const int gx = ((p.e.N + kTcBM - 1) / kTcBM + CN - 1) / CN * CN;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(gx, (p.e.M + BN - 1) / BN);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = L::kTotal;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CN;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tw, tb, p);
+}
+
+template <int WB, int BN, int ST>
+static cudaError_t launch_tc3(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int cn,
+                              cudaStream_t stream) {
+  switch (cn) {
+    case 1: return launch_tc4<WB, BN, ST, 1>(tw, tb, p, stream);
+    case 2: return launch_tc4<WB, BN, ST, 2>(tw, tb, p, stream);
+    default: return launch_tc4<WB, BN, ST, 4>(tw, tb, p, stream);
+  }
 }
 
 template <int WB, int BN>
-static cudaError_t launch_tc2(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int stages,
+static cudaError_t launch_tc2(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int cn,
                               cudaStream_t stream) {
-  switch (stages) {
-    case 2: return launch_tc3<WB, BN, 2>(tw, tb, p, stream);
-    case 3: return launch_tc3<WB, BN, 3>(tw, tb, p, stream);
-    case 4: return launch_tc3<WB, BN, 4>(tw, tb, p, stream);
-    case 5: return launch_tc3<WB, BN, 5>(tw, tb, p, stream);
-    default: return launch_tc3<WB, BN, 6>(tw, tb, p, stream);
-  }
+  return launch_tc3<WB, BN, tc_stages_ct(WB, BN)>(tw, tb, p, cn, stream);
 }
 
 template <int WB>
-static cudaError_t launch_tc1(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int bn, int stages,
+static cudaError_t launch_tc1(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int bn, int cn,
                               cudaStream_t stream) {
-  if (bn == 256) return launch_tc2<WB, 256>(tw, tb, p, stages, stream);
-  return launch_tc2<WB, 128>(tw, tb, p, stages, stream);
+  if (bn == 256) return launch_tc2<WB, 256>(tw, tb, p, cn, stream);
+  return launch_tc2<WB, 128>(tw, tb, p, cn, stream);
 }
 
-cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int stages, void* workspace, cudaStream_t stream) {
+cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, cudaStream_t stream) {
   PFN_encodeTiled_t enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
-  // 1) token expand pre-pass into the workspace
-  {
-    const int64_t total = (int64_t)p.e.M * p.k_words;
-    const int blocks = (int)((total + 255) / 256);
-    expand_tokens_kernel<<<blocks, 256, 0, stream>>>(p.ap, p.a_pstride, p.e.M, p.k_words, p.abits,
-                                                     reinterpret_cast<uint8_t*>(workspace));
-    cudaError_t err = cudaGetLastError();
-    if (err != cudaSuccess) return err;
-  }
-  // 2) tensor maps
   CUtensorMap tw, tb;
   {
     cuuint64_t dims[3] = {(cuuint64_t)p.k_words, (cuuint64_t)p.e.N, (cuuint64_t)wbits};
@@ -382,23 +460,29 @@ cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int stages, void*
     const cuuint64_t kp = (cuuint64_t)p.k_words * 32;
     cuuint64_t dims[2] = {kp, (cuuint64_t)p.e.M};
     cuuint64_t strides[1] = {kp};
-    cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)bn};
+    cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)(bn / cluster_n)};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, workspace, dims, strides, box, es,
+    CUresult r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(p.adig), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
   switch (wbits) {
-    case 1: return launch_tc1<1>(tw, tb, p, bn, stages, stream);
-    case 2: return launch_tc1<2>(tw, tb, p, bn, stages, stream);
-    case 3: return launch_tc1<3>(tw, tb, p, bn, stages, stream);
-    case 4: return launch_tc1<4>(tw, tb, p, bn, stages, stream);
-    case 5: return launch_tc1<5>(tw, tb, p, bn, stages, stream);
-    case 6: return launch_tc1<6>(tw, tb, p, bn, stages, stream);
-    case 7: return launch_tc1<7>(tw, tb, p, bn, stages, stream);
-    default: return launch_tc1<8>(tw, tb, p, bn, stages, stream);
+    case 1: return launch_tc1<1>(tw, tb, p, bn, cluster_n, stream);
+    case 2: return launch_tc1<2>(tw, tb, p, bn, cluster_n, stream);
+    case 3: return launch_tc1<3>(tw, tb, p, bn, cluster_n, stream);
+    case 4: return launch_tc1<4>(tw, tb, p, bn, cluster_n, stream);
+    case 5: return launch_tc1<5>(tw, tb, p, bn, cluster_n, stream);
+    case 6: return launch_tc1<6>(tw, tb, p, bn, cluster_n, stream);
+    case 7: return launch_tc1<7>(tw, tb, p, bn, cluster_n, stream);
+    default: return launch_tc1<8>(tw, tb, p, bn, cluster_n, stream);
   }
 }
 
 }  // namespace apt
+
+#ifdef APT_TC_TRACE
+extern "C" __attribute__((visibility("default"))) int apt_debug_tc_trace(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, apt::g_tc_trace, sizeof(long long) * (n < 8 * 512 ? n : 8 * 512));
+}
+#endif

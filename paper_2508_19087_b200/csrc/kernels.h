@@ -15,21 +15,21 @@ struct PackArgs {
   int64_t plane_stride;  // rows * k_words
   int32_t* row_sum;
   int32_t* range_error;
+  uint8_t* digits;       // optional [rows][Kpad] kernel-order u8 digits
 };
 cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream);
 
 struct MmaArgs {
   const uint32_t* wp;      // weight planes [wbits][N][k_words]
   int64_t w_pstride;       // N * k_words
-  const uint32_t* ap;      // activation planes [abits][M][k_words]
-  int64_t a_pstride;       // M * k_words
+  const uint8_t* adig;     // activation digits [M][Kpad], kernel K order
   int32_t k_words;
-  int32_t abits;
-  int32_t kw_per_split;    // multiple of 8
   EpilogueArgs e;
 };
-cudaError_t launch_gemm_mma(const MmaArgs& p, int wbits, int bn, int split, cudaStream_t stream);
-size_t mma_smem_bytes(int bn, int split);
+cudaError_t launch_gemm_mma(const MmaArgs& p, int wbits, int bn, int warps, cudaStream_t stream);
+// activation planes [abits][M][k_words] -> kernel-order u8 digits [M][Kpad]
+cudaError_t launch_expand_tokens(const uint32_t* ap, int64_t a_pstride, int M, int k_words, int abits,
+                                 uint8_t* out, cudaStream_t stream);
 
 }  // namespace apt
 
@@ -37,13 +37,11 @@ namespace apt {
 struct TcArgs {
   const uint32_t* wp;      // weight planes [wbits][N][k_words]
   int64_t w_pstride;       // N * k_words
-  const uint32_t* ap;      // activation planes [abits][M][k_words]
-  int64_t a_pstride;       // M * k_words
+  const uint8_t* adig;     // activation digits [M][Kpad], kernel K order (TMA source)
   int32_t k_words;
-  int32_t abits;
   EpilogueArgs e;
 };
-cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int stages, void* workspace, cudaStream_t stream);
+cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, cudaStream_t stream);
 int tc_stages(int wbits, int bn);
 size_t tc_workspace_bytes(int M, int k_words);
 }  // namespace apt

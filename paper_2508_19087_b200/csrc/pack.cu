@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(128) pack_kernel(PackArgs p) {
     }
     // planes: bit i of every element, element c -> bit c % 32 (LSB first)
     uint32_t* dst = p.planes + (int64_t)r * p.k_words + w;
+    uint32_t pw[BITS];
 #pragma unroll
     for (int i = 0; i < BITS; ++i) {
       uint32_t word = 0;
@@ -120,6 +121,15 @@ __global__ void __launch_bounds__(128) pack_kernel(PackArgs p) {
         word |= nib << (4 * j);
       }
       dst[(int64_t)i * p.plane_stride] = word;
+      pw[i] = word;
+    }
+    if (p.digits) {
+      // the optional digit view: the same word through the kernels' operand rebuild
+      uint32_t d[8];
+      rebuild8<BITS>(pw, d);
+      uint4* dd = reinterpret_cast<uint4*>(p.digits + ((int64_t)r * p.k_words + w) * 32);
+      dd[0] = make_uint4(d[0], d[1], d[2], d[3]);
+      dd[1] = make_uint4(d[4], d[5], d[6], d[7]);
     }
   }
   // CTA reduction of the row sum (pads contribute 0)

@@ -132,14 +132,49 @@ def test_bound_rejected():
         P.gemm(W, A)
 
 
-@pytest.mark.parametrize("bn,split", [(8, 1), (16, 2), (32, 3), (64, 8), (8, 8)])
-def test_config_invariance(bn, split):
-    """any legal configuration gives identical bits."""
+@pytest.mark.parametrize("bn,split", [(8, 1), (16, 2), (8, 3), (16, 8), (8, 8)])
+def test_config_invariance_decode(bn, split):
+    """any legal configuration gives identical bits (decode kernel tiles / K split)."""
     a = signed_codes(20, 4096, 4, seed=3)
     w = signed_codes(200, 4096, 3, seed=4)
     cfg = P.select_config(20, 200, 4096, 3, 4)
     cfg.update(bn=bn, split_k=split)
     _check_gemm(a, 4, w, 3, config=cfg)
+
+
+@pytest.mark.parametrize("bn,cn", [(128, 1), (128, 2), (128, 4), (256, 1), (256, 2)])
+def test_config_invariance_tc(bn, cn):
+    """S:336 for the tcgen05 kernel: token tile width and cluster multicast do not change the bits."""
+    a = signed_codes(300, 1000, 3, seed=5)
+    w = signed_codes(600, 1000, 5, seed=6)
+    cfg = P.select_config(300, 600, 1000, 5, 3)
+    stage = bn * 128 + 5 * 128 * 16
+    cfg.update(bn=bn, cluster_n=cn, stages=max(2, min(6, ((108 if bn <= 128 else 216) * 1024) // stage)))
+    _check_gemm(a, 3, w, 5, config=cfg)
+
+
+@pytest.mark.parametrize("m,pa,pw", [(1, 2, 1), (16, 4, 3), (300, 8, 2)])
+def test_activation_digit_view(m, pa, pw):
+    """The pack kernel's optional digit view: each 32-element word is a permutation of the word's
+    offset digits u = x + 2^(n-1), and GEMMs reading it equal GEMMs expanding the planes."""
+    k, n = 1000, 96
+    a = signed_codes(m, k, pa, seed=40 + m)
+    w = signed_codes(n, k, pw, seed=41 + m)
+    A = P.pack(_dev(a), pa, digits=True)
+    A0 = P.pack(_dev(a), pa)
+    W = P.pack(_dev(w), pw)
+    dig = A.digits.cpu().numpy().astype(np.int64)
+    kp = O.kpad(k)
+    u = np.zeros((m, kp), dtype=np.int64) + (1 << (pa - 1))
+    u[:, :k] = O.offset_bits_matrix(a, pa)
+    assert dig.shape == (m, kp)
+    assert np.array_equal(np.sort(dig.reshape(m, -1, 32), axis=2), np.sort(u.reshape(m, -1, 32), axis=2))
+    ref = O.gemm_signed(a, w)
+    for kind in ("i32", "bipolar"):
+        g1 = P.gemm(W, A, out_kind=kind).cpu().numpy()
+        g0 = P.gemm(W, A0, out_kind=kind).cpu().numpy()
+        assert np.array_equal(g1, g0)
+    assert np.array_equal(P.gemm(W, A).cpu().numpy().astype(np.int64), ref)
 
 
 # ----------------------------------------------------------------------------- fp16 epilogue (T9)

@@ -52,7 +52,7 @@ def case(m, n, k, wb, ab, cfg=None, baselines=True, tag=""):
     Ws = [P.pack(torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev), wb)
           for _ in range(copies)]
     a = torch.randint(-(1 << (ab - 1)), 1 << (ab - 1), (m, k), dtype=torch.int8, device=dev)
-    A = P.pack(a, ab)
+    A = P.pack(a, ab, digits=True)
     ws = torch.rand(n, device=dev) * 1e-3
     as_ = torch.rand(m, device=dev)
     out = torch.empty((m, n), dtype=torch.float16, device=dev)
