@@ -12,6 +12,7 @@ namespace {
 
 constexpr int kNumSMs = 148;
 
+
 int64_t kpad_of(int64_t k) { return ((k + APT_KPAD_QUANTUM - 1) / APT_KPAD_QUANTUM) * APT_KPAD_QUANTUM; }
 
 bool bound_ok(int64_t k, int wbits, int abits) {
@@ -36,16 +37,21 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
   if (c->w_digit != wbits || c->a_digit != abits) return APT_ERR_UNSUPPORTED;  // full-width digits only
   (void)kw;
   if (c->kernel == APT_KERNEL_MMA_SPLITK) {
-    if (c->bm != 16 || c->bk != 256) return APT_ERR_UNSUPPORTED;
+    if (c->bm != 32 || c->bk != 256) return APT_ERR_UNSUPPORTED;
     if (c->bn != 8 && c->bn != 16) return APT_ERR_UNSUPPORTED;
-    if (c->split_k < 1 || c->split_k > 8) return APT_ERR_UNSUPPORTED;
+    if (c->split_k != 4) return APT_ERR_UNSUPPORTED;
+    if (apt::mma_depth(wbits, abits, c->bn, kw) < 2) return APT_ERR_UNSUPPORTED;
     if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
     return APT_OK;
   }
   if (c->kernel == APT_KERNEL_TC) {
-    if (c->bm != 128 || c->bk != 128 || (c->bn != 128 && c->bn != 256)) return APT_ERR_UNSUPPORTED;
-    if (c->stages != apt::tc_stages(wbits, c->bn) || c->split_k != 1 || c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
+    if (c->bm != 128 || c->bk != 128) return APT_ERR_UNSUPPORTED;
+    if (c->bn != 16 && c->bn != 64 && c->bn != 128 && c->bn != 256) return APT_ERR_UNSUPPORTED;
+    if (c->stages != apt::tc_stages(wbits, c->bn) || c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
     if (c->cluster_n != 1 && c->cluster_n != 2 && c->cluster_n != 4) return APT_ERR_UNSUPPORTED;
+    if (c->split_k < 1 || c->split_k > 8) return APT_ERR_UNSUPPORTED;
+    if (c->split_k > 1 && (c->bn > 64 || c->cluster_n != 1)) return APT_ERR_UNSUPPORTED;
+    if (c->cluster_n > 1 && c->bn < 128) return APT_ERR_UNSUPPORTED;
     return APT_OK;
   }
   return APT_ERR_UNSUPPORTED;
@@ -109,35 +115,38 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
   const int kw = (int)(kpad_of(K) / 32);
   out->w_digit = wbits;
   out->a_digit = abits;
-  if (M > 64) {
-    // prefill: tcgen05 kind::i8, 128 weight rows x 128 tokens per CTA, two CTAs per SM
-    out->kernel = APT_KERNEL_TC;
-    out->bm = 128;
-    out->bn = 128;
-    out->bk = 128;
-    out->stages = apt::tc_stages(wbits, out->bn);
-    out->split_k = 1;
-    out->cta_pair = 0;
-    out->cluster_n = ceil_div(N, 128) >= 4 ? 4 : ceil_div(N, 128) >= 2 ? 2 : 1;
-    return APT_OK;
-  }
-  // decode: 16 weight rows per CTA, K split over 8 warps, tokens in tiles of 8 or 16
-  out->kernel = APT_KERNEL_MMA_SPLITK;
-  out->cluster_n = 1;
-  out->bm = 16;
-  out->bk = 256;
-  out->stages = 2;
+  // every shape runs on the tcgen05 kernel (the mma.sync decode kernel stays selectable by config)
+  out->kernel = APT_KERNEL_TC;
+  out->bm = 128;
+  out->bk = 128;
   out->cta_pair = 0;
-  out->bn = M <= 8 ? 8 : 16;
-  out->split_k = 8;
-  (void)kw;
+  if (M > 64) {
+    // prefill: 128 weight rows x 128 tokens per CTA, two CTAs per SM, the token tile multicast to a
+    // cluster of up to 4 weight tiles
+    out->bn = 128;
+    out->split_k = 1;
+    out->cluster_n = ceil_div(N, 128) >= 4 ? 4 : ceil_div(N, 128) >= 2 ? 2 : 1;
+  } else {
+    // decode: 16 (or 64) tokens per tile, K split over a cluster of up to 8 CTAs so that about two
+    // CTAs per SM stream weights
+    out->bn = M <= 16 ? 16 : 64;
+    out->cluster_n = 1;
+    const int64_t tiles = (int64_t)ceil_div(N, 128) * ceil_div(M, out->bn);
+    const int chunks = (kw / 4 + (wbits <= 4 ? 1 : 0)) / (wbits <= 4 ? 2 : 1);
+    int split = (int)((2 * kNumSMs + tiles / 2) / tiles);
+    if (split > 8) split = 8;
+    if (split > chunks) split = chunks;
+    if (split < 1) split = 1;
+    out->split_k = split;
+  }
+  out->stages = apt::tc_stages(wbits, out->bn);
   return APT_OK;
 }
 
 size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
-  // activation digit view for activations packed without one (apt_packed.digits == NULL)
+  // TC kernel: activation digit view for activations packed without one (apt_packed.digits == NULL)
   (void)N;
-  if (!cfg || M <= 0 || K <= 0) return 0;
+  if (!cfg || M <= 0 || K <= 0 || cfg->kernel != APT_KERNEL_TC) return 0;
   return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
 }
 
@@ -166,7 +175,7 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   }
   st = validate_config(&c, M, N, K, wbits, abits);
   if (st != APT_OK) return st;
-  const size_t need = A->digits ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
+  const size_t need = (A->digits && c.kernel == APT_KERNEL_TC) ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
   if (need > 0 && (!workspace || ws_bytes < need || !aligned16(workspace))) return APT_ERR_WORKSPACE;
   if (A->digits && !aligned16(A->digits)) return APT_ERR_INVALID_ARGUMENT;
 
@@ -186,23 +195,26 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   e.h_w = 1 << (wbits - 1);
   e.h_a = 1 << (abits - 1);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // the activation operand as kernel-order u8 digits: the packed view, or expanded now
+  if (c.kernel == APT_KERNEL_MMA_SPLITK) {
+    apt::MmaArgs p;
+    p.wp = W->planes;
+    p.w_pstride = (int64_t)N * W->k_words;
+    p.ap = A->planes;
+    p.a_pstride = (int64_t)M * A->k_words;
+    p.k_words = W->k_words;
+    p.abits = abits;
+    p.e = e;
+    cudaError_t err = apt::launch_gemm_mma(p, wbits, c.bn, s);
+    return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+  }
+  // the TC kernel reads the activation operand as kernel-order u8 digits: the packed view, or
+  // expanded now into the workspace
   const uint8_t* adig = A->digits;
   if (!adig) {
     cudaError_t err = apt::launch_expand_tokens(A->planes, (int64_t)M * A->k_words, M, A->k_words, abits,
                                                 reinterpret_cast<uint8_t*>(workspace), s);
     if (err != cudaSuccess) return APT_ERR_CUDA;
     adig = reinterpret_cast<const uint8_t*>(workspace);
-  }
-  if (c.kernel == APT_KERNEL_MMA_SPLITK) {
-    apt::MmaArgs p;
-    p.wp = W->planes;
-    p.w_pstride = (int64_t)N * W->k_words;
-    p.adig = adig;
-    p.k_words = W->k_words;
-    p.e = e;
-    cudaError_t err = apt::launch_gemm_mma(p, wbits, c.bn, c.split_k, s);
-    return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   if (c.kernel == APT_KERNEL_TC) {
     apt::TcArgs p;
@@ -211,7 +223,7 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
     p.adig = adig;
     p.k_words = W->k_words;
     p.e = e;
-    cudaError_t err = apt::launch_gemm_tc(p, wbits, c.bn, c.cluster_n, s);
+    cudaError_t err = apt::launch_gemm_tc(p, wbits, c.bn, c.cluster_n, c.split_k, s);
     return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   return APT_ERR_UNSUPPORTED;

@@ -1,37 +1,65 @@
-// gemm_mma.cu — APT W_p x A_q GEMM for small token counts (decode, M <= 64): register rebuild of
-// the weight planes into u8 digit fragments + legacy mma.sync.m16n8k32.u8.u8.s32, K split across the
-// warps of a CTA and reduced through shared memory.
+// gemm_mma.cu — APT W_p x A_q GEMM for small token counts (decode, M <= 64): TMA-streamed weight
+// bit-planes, register rebuild into u8 digit fragments + legacy mma.sync.m16n8k32.u8.u8.s32, K split
+// across the warps of a CTA and reduced through shared memory.
 //
 // Mapping to the paper:
 //   * recovery-oriented scheduling (§4.2 (1)): every plane of a B_M x B_N output block is
 //     consumed in one CTA and nothing per-plane reaches global memory;
-//   * K partitioned into B_K steps (§4.2 (2)) and "weight-bit fragment reuse" (§4.2 (4),
-//     P:276): the weight planes of a 16-row fragment are rebuilt once per K step and reused for every
-//     8-token MMA column tile;
+//   * the unified matrix moves with single commands (§4.1 Step 3): one 3-D TMA box carries all
+//     wbits planes of a 16-row x 256-element weight slab;
+//   * K partitioned into B_K steps with multi-buffered staging (§4.2 (2)/(3)) and
+//     "weight-bit fragment reuse" (§4.2 (4)): a 16-row weight fragment is rebuilt once per K step
+//     and reused for every 8-token MMA column tile; the activation planes of the CTA's tokens are staged
+//     once in shared memory;
 //   * the shift-add of P:228 is folded into the operand rebuild (digit = sum_i 2^i u_i), so each
 //     K=32 step is ONE u8 MMA for any p, q <= 8 instead of p*q 1-bit MMAs (R1);
 //   * the remaining rank-1 terms and the fp16 scale are applied in the epilogue (common.cuh).
 //
-// Decode is a stream over the packed weights, so the kernel is a flat latency chain:
-//   CTA = W warps (W = split_k <= 8) x 16 weight rows (one MMA M tile) x BN = 8*NT tokens.  Warp w owns
-//   a contiguous 1/W of K.  Every lane loads its own 32-byte sector quarter of the plane words of rows
-//   g and g+8 (each packed weight byte is loaded exactly once, straight into registers, one
-//   256-element iteration ahead) and the activation digits (kernel-order u8, L2 resident) for the
-//   same K; it rebuilds the weight fragments with rebuild8() and issues the MMAs.  The W partial
-//   16 x BN tiles are summed through shared memory and stored by the epilogue, whose operands (row
-//   sums, scales) were requested at kernel entry.  No cluster, no global atomics, one __syncthreads.
+// Decode streams the packed weights once and is bound by bytes in flight, so every warp owns a
+// private `depth`-slot TMA ring: CTA = 8 warps = 2 row tiles (16 weight rows, the MMA M side) x 4 K
+// quarters, BN = 8*NT tokens.  Lane 0 of each warp keeps `depth` 256-element slabs of its (row tile,
+// K quarter) in flight (mbarrier complete_tx), refilling a slot as soon as the warp has read it.
+// The four K-quarter partials are summed through shared memory and stored by the epilogue, whose
+// operands were requested at entry.
 //
 // K order inside the MMA: an iteration covers 8 plane words (256 K elements) of a row.  Lane (g, t)
 // owns words 2t (group 0) and 2t+1 (group 1); the 8 digit registers of rebuild8() for a word fill the
-// 4 K=32 steps of its group (reg 2s -> a0/a1/b0, reg 2s+1 -> a2/a3/b1).  The activation digit view is
-// written by the pack kernel (or the expand pre-pass) with the same rebuild8() order, so both
-// operands agree on K.
+// 4 K=32 steps of its group (reg 2s -> a0/a1/b0, reg 2s+1 -> a2/a3/b1).  Tokens go through the same
+// rebuild8() of the same word, so both operands agree on K.
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "kernels.h"
+#include "sync.cuh"
 
 namespace apt {
+
+constexpr int kDecRows = 32;      // weight rows per CTA (2 MMA M tiles)
+constexpr int kDecKq = 4;         // K quarters per CTA
+constexpr int kDecThreads = 256;  // 8 warps
+constexpr int kDecWarps = 8;
+constexpr int kDecMaxSmem = 220 * 1024;
+
+// token-plane row pitch in u32 words: >= k_words and == 8 (mod 32), so the 8 token rows a warp reads
+// with one 64-bit load land in distinct bank groups (2 wavefronts for 256 B, the minimum)
+__host__ __device__ inline int dec_stride(int k_words) { return k_words + ((8 - (k_words & 31)) & 31); }
+
+struct DecSmem {
+  int ring_off, tok_off, red_off, ep_off, bar_off, total;
+};
+
+// rings [8 warps][depth][wbits][16 rows][8 words] | token planes [abits][BN][stride] |
+// partials [4][32][BN] | epilogue operands | mbarriers [8][depth]
+__host__ __device__ inline DecSmem dec_smem_layout(int wbits, int abits, int bn, int k_words, int depth) {
+  DecSmem L;
+  L.ring_off = 0;
+  L.tok_off = L.ring_off + kDecWarps * depth * wbits * 512;
+  L.red_off = L.tok_off + abits * bn * dec_stride(k_words) * 4;
+  L.ep_off = L.red_off + kDecKq * kDecRows * bn * 4;
+  L.bar_off = (L.ep_off + (2 * kDecRows + 2 * bn) * 4 + 7) & ~7;
+  L.total = L.bar_off + kDecWarps * depth * 8;
+  return L;
+}
 
 __device__ __forceinline__ void mma_u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                        uint32_t b0, uint32_t b1) {
@@ -42,15 +70,8 @@ __device__ __forceinline__ void mma_u8(int (&c)[4], uint32_t a0, uint32_t a1, ui
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint2 ldg_stream_v2(const void* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 
 #ifdef APT_MMA_TRACE
@@ -67,154 +88,199 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 template <int WB, int NT>
-struct DecIter {
-  uint2 w0[WB], w1[WB];  // plane words 2t, 2t+1 of rows g and g+8
-  uint4 b[NT][4];        // activation digits of words 2t, 2t+1 (32 B each) for token nt*8+g
-};
-
-template <int WB, int NT>
-__device__ __forceinline__ void dec_load(DecIter<WB, NT>& d, const uint32_t* w0p, const uint32_t* w1p, bool ok0,
-                                         bool ok1, int64_t pstride, const uint8_t* const (&bp)[NT],
-                                         const bool (&bok)[NT], int word0) {
-#pragma unroll
-  for (int i = 0; i < WB; ++i) {
-    d.w0[i] = ok0 ? ldg_stream_v2(w0p + (int64_t)i * pstride + word0) : make_uint2(0, 0);
-    d.w1[i] = ok1 ? ldg_stream_v2(w1p + (int64_t)i * pstride + word0) : make_uint2(0, 0);
-  }
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      d.b[nt][q] = bok[nt] ? ldg_nc_v4(bp[nt] + (size_t)word0 * 32 + 16 * q) : make_uint4(0, 0, 0, 0);
-  }
-}
-
-template <int WB, int NT>
-__global__ void __launch_bounds__(256) gemm_mma_kernel(MmaArgs p) {
+__global__ void __launch_bounds__(kDecThreads) gemm_mma_kernel(const __grid_constant__ CUtensorMap tm_w, MmaArgs p) {
   constexpr int BN = NT * 8;
-  __shared__ int32_t red[8][16][BN];
+  constexpr uint32_t kSlab = WB * 512;  // bytes of one 16-row x 256-element slab, all planes
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int kw = p.k_words;
+  const int D = p.depth;
+  const DecSmem L = dec_smem_layout(WB, p.abits, BN, kw, D);
+  const int stride = dec_stride(kw);
+  uint32_t* sT = reinterpret_cast<uint32_t*>(smem_raw + L.tok_off);
+  int32_t* red = reinterpret_cast<int32_t*>(smem_raw + L.red_off);
+  int32_t* ep_rw = reinterpret_cast<int32_t*>(smem_raw + L.ep_off);
+  float* ep_ws = reinterpret_cast<float*>(ep_rw + kDecRows);
+  int32_t* ep_ra = reinterpret_cast<int32_t*>(ep_ws + kDecRows);
+  float* ep_as = reinterpret_cast<float*>(ep_ra + BN);
 
   MTRACE(0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nwarps = blockDim.x >> 5;
   const int g = lane >> 2, t = lane & 3;
+  const int rt = warp & 1, kq = warp >> 1;  // row tile, K quarter
   const int N = p.e.N, M = p.e.M;
-  const int n0 = blockIdx.x * 16;
+  const int n0 = blockIdx.x * kDecRows;
   const int tok0 = blockIdx.y * BN;
-  const int n_it = p.k_words >> 3;
-  const int it_b = (warp * n_it) / nwarps, it_e = ((warp + 1) * n_it) / nwarps;
-  const int kpad_bytes = p.k_words * 32;
+  const int n_it = kw >> 3;
+  const int it_b = (kq * n_it) / kDecKq, it_e = ((kq + 1) * n_it) / kDecKq;
+  const int n_my = it_e - it_b;
+  const uint32_t ring = smem_u32(smem_raw + L.ring_off) + (uint32_t)(warp * D) * kSlab;
+  const uint32_t bars = smem_u32(smem_raw + L.bar_off) + (uint32_t)(warp * D) * 8u;
 
-  // epilogue operands, requested first (consumed at the very end)
-  const int e_row = tid & 15, e_tok = tid >> 4;  // thread -> (row, token) of the 16 x BN tile
-  const bool e_act = e_tok < BN && n0 + e_row < N && tok0 + e_tok < M;
-  int32_t e_rw = 0, e_ra = 0;
-  float e_ws = 0.f, e_as = 1.f;
-  if (e_act) {
-    e_rw = __ldg(p.e.w_rowsum + n0 + e_row);
-    e_ra = __ldg(p.e.a_rowsum + tok0 + e_tok);
-    if (p.e.kind == 2) {
-      e_ws = __ldg(p.e.w_scale + n0 + e_row);
-      if (p.e.a_scale) e_as = __ldg(p.e.a_scale + tok0 + e_tok);
+  // 1. this warp's weight slabs in flight (TMA, one box = all planes of 16 rows x 256 elements)
+  if (lane == 0) {
+    for (int d = 0; d < D; ++d) mbar_init(bars + 8 * d, 1);
+    fence_proxy_async();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_w) : "memory");
+    for (int j = 0; j < D && j < n_my; ++j) {
+      mbar_expect_tx(bars + 8 * j, kSlab);
+      tma_load_3d(ring + j * kSlab, &tm_w, bars + 8 * j, (it_b + j) * 8, n0 + rt * 16, 0);
     }
   }
-
-  const bool ok0 = n0 + g < N, ok1 = n0 + g + 8 < N;
-  const uint32_t* w0p = p.wp + (int64_t)(ok0 ? n0 + g : 0) * p.k_words + 2 * t;
-  const uint32_t* w1p = p.wp + (int64_t)(ok1 ? n0 + g + 8 : 0) * p.k_words + 2 * t;
-  const uint8_t* bp[NT];
-  bool bok[NT];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int tok = tok0 + nt * 8 + g;
-    bok[nt] = tok < M;
-    bp[nt] = p.adig + (size_t)(bok[nt] ? tok : 0) * kpad_bytes + 2 * t * 32;
+  // 2. the CTA's token planes -> shared memory (cp.async, 16 B chunks), rows beyond M zero-filled
+  {
+    const int chunks_per_row = kw >> 2;
+    const int total = p.abits * BN * chunks_per_row;
+    const uint32_t s_base = smem_u32(sT);
+    for (int c = tid; c < total; c += kDecThreads) {
+      const int row = c / chunks_per_row, ch = c - row * chunks_per_row;  // row = plane * BN + token
+      const int plane = row / BN, tk = row - plane * BN;
+      const int tok = tok0 + tk;
+      const uint32_t* src = p.ap + (int64_t)plane * p.a_pstride + (int64_t)(tok < M ? tok : 0) * kw + 4 * ch;
+      cp_async16(s_base + (uint32_t)((row * stride + 4 * ch) * 4), src, tok < M ? 16u : 0u);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  // 3. epilogue operands
+  if (tid < kDecRows) {
+    const int n = min(n0 + tid, N - 1);
+    ep_rw[tid] = __ldg(p.e.w_rowsum + n);
+    ep_ws[tid] = p.e.kind == 2 ? __ldg(p.e.w_scale + n) : 0.f;
+  } else if (tid - kDecRows < BN) {
+    const int m = min(tok0 + tid - kDecRows, M - 1);
+    ep_ra[tid - kDecRows] = __ldg(p.e.a_rowsum + m);
+    ep_as[tid - kDecRows] = (p.e.kind == 2 && p.e.a_scale) ? __ldg(p.e.a_scale + m) : 1.f;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  MTRACE(1);
 
   int acc[NT][4];
 #pragma unroll
   for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
 
-  DecIter<WB, NT> cur, nxt;
-  if (it_b < it_e) dec_load<WB, NT>(cur, w0p, w1p, ok0, ok1, p.w_pstride, bp, bok, it_b * 8);
-  MTRACE(1);
-  for (int it = it_b; it < it_e; ++it) {
-    if (it + 1 < it_e) dec_load<WB, NT>(nxt, w0p, w1p, ok0, ok1, p.w_pstride, bp, bok, (it + 1) * 8);
+  for (int j = 0; j < n_my; ++j) {
+    const int it = it_b + j;
+    const int slot = j % D;
+    mbar_wait(bars + 8 * slot, (uint32_t)((j / D) & 1));
+    // weight words 2t, 2t+1 of rows g and g+8 of every plane (conflict-free 64-bit reads)
+    const uint8_t* sl = smem_raw + L.ring_off + (size_t)(warp * D + slot) * kSlab;
+    uint2 w0[WB], w1[WB];
+#pragma unroll
+    for (int i = 0; i < WB; ++i) {
+      w0[i] = *reinterpret_cast<const uint2*>(sl + (i * 16 + g) * 32 + 8 * t);
+      w1[i] = *reinterpret_cast<const uint2*>(sl + (i * 16 + g + 8) * 32 + 8 * t);
+    }
+    __syncwarp();
+    if (lane == 0 && j + D < n_my) {  // refill the slot this warp just drained
+      fence_proxy_async();
+      mbar_expect_tx(bars + 8 * slot, kSlab);
+      tma_load_3d(ring + slot * kSlab, &tm_w, bars + 8 * slot, (it + D) * 8, n0 + rt * 16, 0);
+    }
+    // token fragments: words 2t, 2t+1 of token nt*8+g, every plane, rebuilt to digits
+    uint32_t tb[NT][2][8];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      uint32_t lo[8], hi[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < p.abits) {
+          const uint2 v = *reinterpret_cast<const uint2*>(sT + (i * BN + nt * 8 + g) * stride + it * 8 + 2 * t);
+          lo[i] = v.x;
+          hi[i] = v.y;
+        } else {
+          lo[i] = hi[i] = 0u;
+        }
+      }
+      rebuild8_rt(lo, p.abits, tb[nt][0]);
+      rebuild8_rt(hi, p.abits, tb[nt][1]);
+    }
 #pragma unroll
     for (int gr = 0; gr < 2; ++gr) {
       uint32_t wa[WB], wb[WB], ra[8], rb[8];
 #pragma unroll
       for (int i = 0; i < WB; ++i) {
-        wa[i] = gr ? cur.w0[i].y : cur.w0[i].x;
-        wb[i] = gr ? cur.w1[i].y : cur.w1[i].x;
+        wa[i] = gr ? w0[i].y : w0[i].x;
+        wb[i] = gr ? w1[i].y : w1[i].x;
       }
       rebuild8<WB>(wa, ra);
       rebuild8<WB>(wb, rb);
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          // digits of word 2t+gr, registers 2s and 2s+1: uint4 index gr*2 + s/2, components (s%2)*2, +1
-          const uint4 q = cur.b[nt][gr * 2 + (s >> 1)];
-          const uint32_t b0 = (s & 1) ? q.z : q.x;
-          const uint32_t b1 = (s & 1) ? q.w : q.y;
-          mma_u8(acc[nt], ra[2 * s], rb[2 * s], ra[2 * s + 1], rb[2 * s + 1], b0, b1);
-        }
+        for (int nt = 0; nt < NT; ++nt)
+          mma_u8(acc[nt], ra[2 * s], rb[2 * s], ra[2 * s + 1], rb[2 * s + 1], tb[nt][gr][2 * s],
+                 tb[nt][gr][2 * s + 1]);
       }
     }
-    if (it + 1 < it_e) cur = nxt;
   }
   MTRACE(2);
 
-  // ---- reduction of the per-warp K partials through shared memory
+  // ---- the four K-quarter partials meet in shared memory
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int tk = nt * 8 + 2 * t;
-    red[warp][g][tk] = acc[nt][0];
-    red[warp][g][tk + 1] = acc[nt][1];
-    red[warp][g + 8][tk] = acc[nt][2];
-    red[warp][g + 8][tk + 1] = acc[nt][3];
+    const int lr = rt * 16 + g;
+    red[(kq * kDecRows + lr) * BN + tk] = acc[nt][0];
+    red[(kq * kDecRows + lr) * BN + tk + 1] = acc[nt][1];
+    red[(kq * kDecRows + lr + 8) * BN + tk] = acc[nt][2];
+    red[(kq * kDecRows + lr + 8) * BN + tk + 1] = acc[nt][3];
   }
   __syncthreads();
   MTRACE(3);
-  if (e_act) {
-    uint32_t U = 0;
-    for (int w = 0; w < nwarps; ++w) U += (uint32_t)red[w][e_row][e_tok];
-    epilogue_store_v(p.e, tok0 + e_tok, n0 + e_row, U, e_ra, e_rw, e_ws, e_as);
+  for (int idx = tid; idx < kDecRows * BN; idx += kDecThreads) {
+    int lr, tk;
+    if (p.e.layout == 0) { lr = idx % kDecRows; tk = idx / kDecRows; }  // consecutive rows n -> coalesced
+    else { tk = idx % BN; lr = idx / BN; }                            // consecutive tokens m -> coalesced
+    const int n = n0 + lr, m = tok0 + tk;
+    if (n < N && m < M) {
+      uint32_t U = 0;
+#pragma unroll
+      for (int q = 0; q < kDecKq; ++q) U += (uint32_t)red[(q * kDecRows + lr) * BN + tk];
+      epilogue_store_v(p.e, m, n, U, ep_ra[tk], ep_rw[lr], ep_ws[lr], ep_as[tk]);
+    }
   }
   MTRACE(4);
 }
 
+// deepest per-warp ring (2..8 slabs) that fits next to the token planes; 0 if even 2 do not fit
+int mma_depth(int wbits, int abits, int bn, int k_words) {
+  for (int d = 8; d >= 2; --d)
+    if (dec_smem_layout(wbits, abits, bn, k_words, d).total <= kDecMaxSmem) return d;
+  return 0;
+}
+
 template <int WB, int NT>
-static cudaError_t launch_one(const MmaArgs& p, int warps, cudaStream_t stream) {
-  dim3 grid((p.e.N + 15) / 16, (p.e.M + NT * 8 - 1) / (NT * 8));
-  gemm_mma_kernel<WB, NT><<<grid, 32 * warps, 0, stream>>>(p);
+static cudaError_t launch_one(const CUtensorMap& tw, const MmaArgs& p, cudaStream_t stream) {
+  const int smem = dec_smem_layout(WB, p.abits, NT * 8, p.k_words, p.depth).total;
+  auto kern = gemm_mma_kernel<WB, NT>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err != cudaSuccess) return err;
+  dim3 grid((p.e.N + kDecRows - 1) / kDecRows, (p.e.M + NT * 8 - 1) / (NT * 8));
+  kern<<<grid, kDecThreads, smem, stream>>>(tw, p);
   return cudaGetLastError();
 }
 
 template <int WB>
-static cudaError_t launch_wb(const MmaArgs& p, int nt, int warps, cudaStream_t stream) {
-  switch (nt) {
-    case 1: return launch_one<WB, 1>(p, warps, stream);
-    case 2: return launch_one<WB, 2>(p, warps, stream);
-    case 4: return launch_one<WB, 4>(p, warps, stream);
-    default: return launch_one<WB, 8>(p, warps, stream);
-  }
+static cudaError_t launch_wb(const CUtensorMap& tw, const MmaArgs& p, int nt, cudaStream_t stream) {
+  return nt == 1 ? launch_one<WB, 1>(tw, p, stream) : launch_one<WB, 2>(tw, p, stream);
 }
 
-cudaError_t launch_gemm_mma(const MmaArgs& p, int wbits, int bn, int warps, cudaStream_t stream) {
+cudaError_t launch_gemm_mma(const MmaArgs& p_in, int wbits, int bn, cudaStream_t stream) {
+  MmaArgs p = p_in;
+  p.depth = mma_depth(wbits, p.abits, bn, p.k_words);
+  if (p.depth < 2) return cudaErrorInvalidConfiguration;
+  CUtensorMap tw;
+  if (!make_plane_map(&tw, p.wp, p.k_words, p.e.N, wbits, 8, 16)) return cudaErrorInvalidValue;
   const int nt = bn / 8;
-  // the epilogue maps one thread per (row, token) of the 16 x BN tile
-  if (warps * 32 < 16 * bn) warps = (16 * bn) / 32;
   switch (wbits) {
-    case 1: return launch_wb<1>(p, nt, warps, stream);
-    case 2: return launch_wb<2>(p, nt, warps, stream);
-    case 3: return launch_wb<3>(p, nt, warps, stream);
-    case 4: return launch_wb<4>(p, nt, warps, stream);
-    case 5: return launch_wb<5>(p, nt, warps, stream);
-    case 6: return launch_wb<6>(p, nt, warps, stream);
-    case 7: return launch_wb<7>(p, nt, warps, stream);
-    default: return launch_wb<8>(p, nt, warps, stream);
+    case 1: return launch_wb<1>(tw, p, nt, stream);
+    case 2: return launch_wb<2>(tw, p, nt, stream);
+    case 3: return launch_wb<3>(tw, p, nt, stream);
+    case 4: return launch_wb<4>(tw, p, nt, stream);
+    case 5: return launch_wb<5>(tw, p, nt, stream);
+    case 6: return launch_wb<6>(tw, p, nt, stream);
+    case 7: return launch_wb<7>(tw, p, nt, stream);
+    default: return launch_wb<8>(tw, p, nt, stream);
   }
 }
 

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.h"
+#include "sync.cuh"
 
 namespace apt {
 
@@ -42,36 +43,6 @@ __device__ long long g_tc_trace[8][512];
 #endif
 
 // ------------------------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-      "l"(map), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
@@ -151,13 +122,19 @@ cudaError_t launch_expand_tokens(const uint32_t* ap, int64_t a_pstride, int M, i
 // ------------------------------------------------------------------------------------ main kernel
 template <int WB, int BN, int STAGES>
 struct TcSmem {
-  static constexpr int kBBytes = BN * kTcBK;            // token digits per stage
-  static constexpr int kWBytes = WB * kTcBM * 16;       // weight planes per stage (4 words per row per plane)
+  // weight planes move in chunks of CW words (CW*32 K elements) per row and plane (32-byte TMA rows
+  // for WB <= 4); decode-sized tiles keep more chunks in flight (HBM latency x bandwidth)
+  static constexpr int kCW = WB <= 4 ? 8 : 4;
+  static constexpr int kKpc = kCW / 4;                  // 128-element K steps per weight chunk
+  static constexpr int kWSlots = BN <= 64 ? 6 : 2;
+  static constexpr int kBBytes = BN * kTcBK;            // token digits per K step
+  static constexpr int kWBytes = WB * kTcBM * kCW * 4;  // weight planes per chunk
   static constexpr int kBOff = 0;
   static constexpr int kWOff = STAGES * kBBytes;
-  static constexpr int kEpOff = kWOff + STAGES * kWBytes;  // rw[128] ws[128] ra[BN] as[BN]
+  static constexpr int kRbOff = kWOff + kWSlots * kWBytes;       // split-K receive buffer [128][BN] i32
+  static constexpr int kEpOff = kRbOff + (BN <= 64 ? kTcBM * BN * 4 : 0);  // rw[128] ws[128] ra[BN] as[BN]
   static constexpr int kBarOff = kEpOff + (2 * kTcBM + 2 * BN) * 4;
-  static constexpr int kNumBars = 2 * STAGES + 2 * kTcAStages + 1;
+  static constexpr int kNumBars = 2 * STAGES + 2 * kWSlots + 2 * kTcAStages + 1;
   static constexpr int kTotal = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
 };
 
@@ -175,9 +152,20 @@ __device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 
 // CN = CTAs of a cluster along the weight-row dimension sharing one token tile: each loads BN/CN
 // token rows and multicasts them to all CN, so the token tile crosses L2 -> SM once per cluster.
+// gridDim.z = S > 1 (with CN = 1): the K steps are split over a (1, 1, S) cluster and the S partial
+// accumulator tiles are reduced through distributed shared memory (decode-sized token counts).
 template <int WB, int BN, int STAGES, int CN>
 __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w,
                                                          const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
@@ -189,15 +177,18 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
   const uint32_t sB = base + L::kBOff;
   const uint32_t sW = base + L::kWOff;
   const uint32_t bars = base + L::kBarOff;
+  int32_t* rbuf = reinterpret_cast<int32_t*>(gbase + L::kRbOff);
   int32_t* ep_rw = reinterpret_cast<int32_t*>(gbase + L::kEpOff);
   float* ep_ws = reinterpret_cast<float*>(ep_rw + kTcBM);
   int32_t* ep_ra = reinterpret_cast<int32_t*>(ep_ws + kTcBM);
   float* ep_as = reinterpret_cast<float*>(ep_ra + BN);
   auto full = [&](int s) { return bars + 8u * s; };
   auto empty = [&](int s) { return bars + 8u * (STAGES + s); };
-  auto a_full = [&](int a) { return bars + 8u * (2 * STAGES + a); };
-  auto a_empty = [&](int a) { return bars + 8u * (2 * STAGES + kTcAStages + a); };
-  const uint32_t acc_full = bars + 8u * (2 * STAGES + 2 * kTcAStages);
+  auto wfull = [&](int c) { return bars + 8u * (2 * STAGES + c); };
+  auto wempty = [&](int c) { return bars + 8u * (2 * STAGES + L::kWSlots + c); };
+  auto a_full = [&](int a) { return bars + 8u * (2 * STAGES + 2 * L::kWSlots + a); };
+  auto a_empty = [&](int a) { return bars + 8u * (2 * STAGES + 2 * L::kWSlots + kTcAStages + a); };
+  const uint32_t acc_full = bars + 8u * (2 * STAGES + 2 * L::kWSlots + 2 * kTcAStages);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::kBarOff + L::kNumBars * 8);
   constexpr uint32_t kTmemCols = (BN + 32 * kTcAStages) <= 256 ? 256 : 512;
   constexpr uint32_t kAcol0 = BN;  // A ring after the accumulator columns
@@ -207,14 +198,24 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * kTcBM;   // weight rows
   const int m0 = blockIdx.y * BN;      // tokens
-  const int nk = p.k_words / 4;        // 128-element K steps
-  const uint32_t crank = CN > 1 ? cluster_ctarank() : 0u;
+  const int S = gridDim.z;             // K split (cluster along z)
+  const uint32_t crank = (CN > 1 || S > 1) ? cluster_ctarank() : 0u;
+  // this CTA's K steps, in whole weight chunks
+  const int nk = p.k_words / 4;
+  const int nch = (nk + L::kKpc - 1) / L::kKpc;
+  const int kb = min(nk, (int)((blockIdx.z * nch) / S) * L::kKpc);
+  const int ke = min(nk, (int)(((blockIdx.z + 1) * nch) / S) * L::kKpc);
+  const int nloc = ke - kb;
   if (threadIdx.x == 0) TRACE(6, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(empty(s), CN + 4);   // every CTA's MMA commit (multicast) + the 4 local converter warps
+      mbar_init(empty(s), CN);      // every cluster CTA's MMA commit (multicast when CN > 1)
+    }
+    for (int c = 0; c < L::kWSlots; ++c) {
+      mbar_init(wfull(c), 1);
+      mbar_init(wempty(c), 4);      // the 4 converter warps
     }
     for (int a = 0; a < kTcAStages; ++a) {
       mbar_init(a_full(a), 4);
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  if (CN > 1) cluster_sync_all(); else __syncthreads();
+  if (CN > 1 || S > 1) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
   if (threadIdx.x == 0) TRACE(6, 1);
@@ -242,19 +243,24 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      constexpr uint32_t kTx = L::kBBytes + L::kWBytes;
-      for (int ks = 0; ks < nk; ++ks) {
-        const int s = ks % STAGES;
-        const uint32_t ph = (ks / STAGES) & 1;
+      for (int j = 0; j < nloc; ++j) {
+        const int ks = kb + j;
+        if (j % L::kKpc == 0) {  // next weight chunk: all planes of 128 rows x kCW words, one box
+          const int c = j / L::kKpc;
+          mbar_wait(wempty(c % L::kWSlots), ((c / L::kWSlots) & 1) ^ 1);
+          mbar_expect_tx(wfull(c % L::kWSlots), L::kWBytes);
+          tma_load_3d(sW + (c % L::kWSlots) * L::kWBytes, &tm_w, wfull(c % L::kWSlots), ks * 4, n0, 0);
+        }
+        const int s = j % STAGES;
+        const uint32_t ph = (j / STAGES) & 1;
         mbar_wait(empty(s), ph ^ 1);
-        TRACE(0, ks);
-        mbar_expect_tx(full(s), kTx);
+        TRACE(0, j);
+        mbar_expect_tx(full(s), L::kBBytes);
         const uint32_t dstB = sB + s * L::kBBytes + crank * kRowsPerCta * kTcBK;
         if (CN > 1)
           tma_load_2d_mc(dstB, &tm_b, full(s), ks * kTcBK, m0 + (int)crank * kRowsPerCta, kMask);
         else
           tma_load_2d(dstB, &tm_b, full(s), ks * kTcBK, m0);
-        tma_load_3d(sW + s * L::kWBytes, &tm_w, full(s), ks * 4, n0, 0);
       }
     }
   } else if (warp == 1) {
@@ -263,21 +269,21 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
       constexpr uint32_t idesc = (2u << 4)                       // D = s32
                                  | ((uint32_t)(BN >> 3) << 17)   // N
                                  | ((uint32_t)(kTcBM >> 4) << 24);  // M ; A, B = u8, K-major
-      for (int ks = 0; ks < nk; ++ks) {
-        const int s = ks % STAGES;
-        const uint32_t ph = (ks / STAGES) & 1;
-        const int a = ks % kTcAStages;
-        const uint32_t pa = (ks / kTcAStages) & 1;
+      for (int j = 0; j < nloc; ++j) {
+        const int s = j % STAGES;
+        const uint32_t ph = (j / STAGES) & 1;
+        const int a = j % kTcAStages;
+        const uint32_t pa = (j / kTcAStages) & 1;
         mbar_wait(full(s), ph);
-        TRACE(1, ks);
+        TRACE(1, j);
         mbar_wait(a_full(a), pa);
-        TRACE(2, ks);
+        TRACE(2, j);
         tc_fence_after();
         const uint64_t bdesc = umma_desc_sw128(sB + s * L::kBBytes);
 #pragma unroll
         for (int kk = 0; kk < kTcBK / 32; ++kk) {
           // advance 32 K bytes inside the 128-byte swizzle atom: +2 in the (addr >> 4) field
-          tc_mma_i8(tmem, tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk), idesc, (ks | kk) != 0);
+          tc_mma_i8(tmem, tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk), idesc, (j | kk) != 0);
         }
         if (CN > 1) tc_commit_mc(empty(s), kMask); else tc_commit(empty(s));
         tc_commit(a_empty(a));
@@ -303,29 +309,33 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
     const int sub = warp - 4;            // TMEM sub-partition (lanes 32*sub ..)
     const int r = sub * 32 + lane;       // row within the tile
     const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
-    for (int ks = 0; ks < nk; ++ks) {
-      const int s = ks % STAGES;
-      const uint32_t ph = (ks / STAGES) & 1;
-      mbar_wait(full(s), ph);
-      if (lane == 0 && sub == 0) TRACE(3, ks);
+    for (int j = 0; j < nloc; ++j) {
+      const int c = j / L::kKpc, q = j % L::kKpc;
+      if (q == 0) {
+        mbar_wait(wfull(c % L::kWSlots), (c / L::kWSlots) & 1);
+        if (lane == 0 && sub == 0) TRACE(3, j);
+      }
       uint4 v[WB];
-      const uint4* wsm = reinterpret_cast<const uint4*>(gbase + L::kWOff + s * L::kWBytes);
+      const uint8_t* wsm = gbase + L::kWOff + (c % L::kWSlots) * L::kWBytes;
 #pragma unroll
-      for (int i = 0; i < WB; ++i) v[i] = wsm[i * kTcBM + r];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty(s));
+      for (int i = 0; i < WB; ++i)
+        v[i] = *reinterpret_cast<const uint4*>(wsm + ((i * kTcBM + r) * L::kCW + 4 * q) * 4);
+      if (q == L::kKpc - 1 || j == nloc - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(wempty(c % L::kWSlots));
+      }
       uint32_t d[32];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int jj = 0; jj < 4; ++jj) {
         uint32_t w[WB], o[8];
 #pragma unroll
-        for (int i = 0; i < WB; ++i) w[i] = j == 0 ? v[i].x : j == 1 ? v[i].y : j == 2 ? v[i].z : v[i].w;
+        for (int i = 0; i < WB; ++i) w[i] = jj == 0 ? v[i].x : jj == 1 ? v[i].y : jj == 2 ? v[i].z : v[i].w;
         rebuild8<WB>(w, o);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) d[8 * j + c] = o[c];
+        for (int cc = 0; cc < 8; ++cc) d[8 * jj + cc] = o[cc];
       }
-      const int a = ks % kTcAStages;
-      const uint32_t pa = (ks / kTcAStages) & 1;
+      const int a = j % kTcAStages;
+      const uint32_t pa = (j / kTcAStages) & 1;
       mbar_wait(a_empty(a), pa ^ 1);
       tc_fence_after();
       tmem_st32<32>(tmem + lane_off + kAcol0 + 32 * a, d);
@@ -333,7 +343,7 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full(a));
-      if (lane == 0 && sub == 0) TRACE(4, ks);
+      if (lane == 0 && sub == 0) TRACE(4, j);
     }
     // ------------------------------------------------------------ epilogue
     asm volatile("bar.sync 1, 192;" ::: "memory");   // epilogue operands are in shared memory
@@ -343,15 +353,67 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
     const int n = n0 + r;
     const int32_t rw = ep_rw[r];
     const float wsc = ep_ws[r];
+    if (S == 1) {
+      if constexpr (BN % 32 == 0) {
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t acc[32];
-      tmem_ld32(tmem + lane_off + c0, acc);
-      if (n < p.e.N) {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t acc[32];
+          tmem_ld32(tmem + lane_off + c0, acc);
+          if (n < p.e.N) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int m = m0 + c0 + j;
-          if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[j], ep_ra[c0 + j], rw, wsc, ep_as[c0 + j]);
+            for (int jj = 0; jj < 32; ++jj) {
+              const int m = m0 + c0 + jj;
+              if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[jj], ep_ra[c0 + jj], rw, wsc, ep_as[c0 + jj]);
+            }
+          }
+        }
+      } else {
+        uint32_t acc[16];
+        tmem_ld16(tmem + lane_off, acc);
+        if (n < p.e.N) {
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const int m = m0 + jj;
+            if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[jj], ep_ra[jj], rw, wsc, ep_as[jj]);
+          }
+        }
+      }
+    }
+  }
+  if (BN <= 64 && S > 1) {
+    // ------------------------------------------------------------ split-K reduction over the cluster
+    // converter/epilogue warps push their row's partial of token column c to rank c % S; one cluster
+    // barrier; every rank sums its columns and stores them
+    const int slots = (BN + S - 1) / S;
+    if (warp >= 4) {
+      const int r = (warp - 4) * 32 + lane;
+      const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+      const uint32_t rb_local = smem_u32(rbuf);
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t acc[16];
+        tmem_ld16(tmem + lane_off + c0, acc);
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int col = c0 + jj;
+          const uint32_t off = (uint32_t)((((int)crank * kTcBM + r) * slots + col / S) * 4);
+          uint32_t remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(rb_local + off), "r"(col % S));
+          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(remote), "r"(acc[jj]) : "memory");
+        }
+      }
+    }
+    cluster_sync_all();
+    if (warp >= 4) {
+      const int r = (warp - 4) * 32 + lane;
+      const int n = n0 + r;
+      for (int sl = 0; sl < slots; ++sl) {
+        const int col = (int)crank + S * sl;
+        const int m = m0 + col;
+        if (col < BN && m < p.e.M && n < p.e.N) {
+          uint32_t U = 0;
+          for (int src = 0; src < S; ++src) U += (uint32_t)rbuf[(src * kTcBM + r) * slots + sl];
+          epilogue_store_v(p.e, m, n, U, ep_ra[col], ep_rw[r], ep_ws[r], ep_as[col]);
         }
       }
     }
@@ -368,11 +430,7 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
 }
 
 // ------------------------------------------------------------------------------------ host side
-typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static PFN_encodeTiled_t get_encode() {
+PFN_encodeTiled_t tensor_map_encoder() {
   static PFN_encodeTiled_t fn = nullptr;
   if (!fn) {
     void* ptr = nullptr;
@@ -384,13 +442,28 @@ static PFN_encodeTiled_t get_encode() {
   return fn;
 }
 
+bool make_plane_map(CUtensorMap* map, const uint32_t* planes, int k_words, int rows, int bits, int box_words,
+                    int box_rows) {
+  PFN_encodeTiled_t enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)k_words, (cuuint64_t)rows, (cuuint64_t)bits};
+  cuuint64_t strides[2] = {(cuuint64_t)k_words * 4, (cuuint64_t)k_words * 4 * (cuuint64_t)rows};
+  cuuint32_t box[3] = {(cuuint32_t)box_words, (cuuint32_t)box_rows, (cuuint32_t)bits};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(planes), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+__host__ __device__ constexpr int tc_clamp(int v, int lo, int hi) { return v < lo ? lo : v > hi ? hi : v; }
+
 __host__ __device__ constexpr int tc_stages_ct(int wbits, int bn) {
-  // as deep as shared memory allows: ~108 KB per CTA at BN = 128 (two CTAs per SM), ~216 KB at 256
-  return ((bn <= 128 ? 108 : 216) * 1024) / (bn * kTcBK + wbits * kTcBM * 16) > 6
-             ? 6
-             : ((bn <= 128 ? 108 : 216) * 1024) / (bn * kTcBK + wbits * kTcBM * 16) < 2
-                   ? 2
-                   : ((bn <= 128 ? 108 : 216) * 1024) / (bn * kTcBK + wbits * kTcBM * 16);
+  // token-tile ring as deep as shared memory allows next to the weight-chunk ring: ~108 KB per CTA
+  // at BN <= 128 (two CTAs per SM), ~216 KB at 256
+  return tc_clamp(((bn <= 128 ? 108 : 216) * 1024 -
+                   (bn <= 64 ? 6 : 2) * wbits * kTcBM * (wbits <= 4 ? 8 : 4) * 4 -
+                   (bn <= 64 ? kTcBM * bn * 4 : 0) - 4096) / (bn * kTcBK),
+                  2, 8);
 }
 
 int tc_stages(int wbits, int bn) { return tc_stages_ct(wbits, bn); }
@@ -398,14 +471,15 @@ int tc_stages(int wbits, int bn) { return tc_stages_ct(wbits, bn); }
 size_t tc_workspace_bytes(int M, int k_words) { return (size_t)M * (size_t)k_words * 32u; }
 
 template <int WB, int BN, int ST, int CN>
-static cudaError_t launch_tc4(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, cudaStream_t stream) {
+static cudaError_t launch_tc4(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int split,
+                              cudaStream_t stream) {
   using L = TcSmem<WB, BN, ST>;
   auto kern = gemm_tc_kernel<WB, BN, ST, CN>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
   if (err != cudaSuccess) return err;
   const int gx = ((p.e.N + kTcBM - 1) / kTcBM + CN - 1) / CN * CN;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(gx, (p.e.M + BN - 1) / BN);
+  cfg.gridDim = dim3(gx, (p.e.M + BN - 1) / BN, split);
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = L::kTotal;
   cfg.stream = stream;
@@ -413,49 +487,44 @@ static cudaError_t launch_tc4(const CUtensorMap& tw, const CUtensorMap& tb, cons
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CN;
   attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].val.clusterDim.z = split;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, tw, tb, p);
 }
 
-template <int WB, int BN, int ST>
-static cudaError_t launch_tc3(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int cn,
-                              cudaStream_t stream) {
-  switch (cn) {
-    case 1: return launch_tc4<WB, BN, ST, 1>(tw, tb, p, stream);
-    case 2: return launch_tc4<WB, BN, ST, 2>(tw, tb, p, stream);
-    default: return launch_tc4<WB, BN, ST, 4>(tw, tb, p, stream);
-  }
-}
-
 template <int WB, int BN>
-static cudaError_t launch_tc2(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int cn,
+static cudaError_t launch_tc2(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int cn, int split,
                               cudaStream_t stream) {
-  return launch_tc3<WB, BN, tc_stages_ct(WB, BN)>(tw, tb, p, cn, stream);
+  constexpr int ST = tc_stages_ct(WB, BN);
+  if constexpr (BN < 128) {
+    return launch_tc4<WB, BN, ST, 1>(tw, tb, p, split, stream);
+  } else {
+    switch (cn) {
+      case 1: return launch_tc4<WB, BN, ST, 1>(tw, tb, p, split, stream);
+      case 2: return launch_tc4<WB, BN, ST, 2>(tw, tb, p, split, stream);
+      default: return launch_tc4<WB, BN, ST, 4>(tw, tb, p, split, stream);
+    }
+  }
 }
 
 template <int WB>
 static cudaError_t launch_tc1(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int bn, int cn,
-                              cudaStream_t stream) {
-  if (bn == 256) return launch_tc2<WB, 256>(tw, tb, p, cn, stream);
-  return launch_tc2<WB, 128>(tw, tb, p, cn, stream);
+                              int split, cudaStream_t stream) {
+  switch (bn) {
+    case 16: return launch_tc2<WB, 16>(tw, tb, p, cn, split, stream);
+    case 64: return launch_tc2<WB, 64>(tw, tb, p, cn, split, stream);
+    case 256: return launch_tc2<WB, 256>(tw, tb, p, cn, split, stream);
+    default: return launch_tc2<WB, 128>(tw, tb, p, cn, split, stream);
+  }
 }
 
-cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, cudaStream_t stream) {
-  PFN_encodeTiled_t enc = get_encode();
+cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, int split, cudaStream_t stream) {
+  PFN_encodeTiled_t enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tw, tb;
-  {
-    cuuint64_t dims[3] = {(cuuint64_t)p.k_words, (cuuint64_t)p.e.N, (cuuint64_t)wbits};
-    cuuint64_t strides[2] = {(cuuint64_t)p.k_words * 4, (cuuint64_t)p.w_pstride * 4};
-    cuuint32_t box[3] = {4, (cuuint32_t)kTcBM, (cuuint32_t)wbits};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(p.wp), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  }
+  const int cw = wbits <= 4 ? 8 : 4;
+  if (!make_plane_map(&tw, p.wp, p.k_words, p.e.N, wbits, cw, kTcBM)) return cudaErrorInvalidValue;
   {
     const cuuint64_t kp = (cuuint64_t)p.k_words * 32;
     cuuint64_t dims[2] = {kp, (cuuint64_t)p.e.M};
@@ -468,14 +537,14 @@ cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, cu
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
   switch (wbits) {
-    case 1: return launch_tc1<1>(tw, tb, p, bn, cluster_n, stream);
-    case 2: return launch_tc1<2>(tw, tb, p, bn, cluster_n, stream);
-    case 3: return launch_tc1<3>(tw, tb, p, bn, cluster_n, stream);
-    case 4: return launch_tc1<4>(tw, tb, p, bn, cluster_n, stream);
-    case 5: return launch_tc1<5>(tw, tb, p, bn, cluster_n, stream);
-    case 6: return launch_tc1<6>(tw, tb, p, bn, cluster_n, stream);
-    case 7: return launch_tc1<7>(tw, tb, p, bn, cluster_n, stream);
-    default: return launch_tc1<8>(tw, tb, p, bn, cluster_n, stream);
+    case 1: return launch_tc1<1>(tw, tb, p, bn, cluster_n, split, stream);
+    case 2: return launch_tc1<2>(tw, tb, p, bn, cluster_n, split, stream);
+    case 3: return launch_tc1<3>(tw, tb, p, bn, cluster_n, split, stream);
+    case 4: return launch_tc1<4>(tw, tb, p, bn, cluster_n, split, stream);
+    case 5: return launch_tc1<5>(tw, tb, p, bn, cluster_n, split, stream);
+    case 6: return launch_tc1<6>(tw, tb, p, bn, cluster_n, split, stream);
+    case 7: return launch_tc1<7>(tw, tb, p, bn, cluster_n, split, stream);
+    default: return launch_tc1<8>(tw, tb, p, bn, cluster_n, split, stream);
   }
 }
 

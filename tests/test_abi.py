@@ -59,11 +59,14 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab):
     kw = -(-K // 256) * 8
     assert c.w_digit == wb and c.a_digit == ab
     if c.kernel == L.APT_KERNEL_MMA_SPLITK:
-        assert c.bm == 16 and c.bn in (8, 16) and c.bn >= min(M, 16)
-        assert 1 <= c.split_k <= 8 and c.cluster_n == 1
+        assert c.bm == 32 and c.bn in (8, 16) and c.bn >= min(M, 16)
+        assert c.split_k == 4 and c.cluster_n == 1
     else:
-        assert c.kernel == L.APT_KERNEL_TC and M > 64
-        assert c.bm == 128 and c.bn in (128, 256) and c.cluster_n in (1, 2, 4) and c.split_k == 1
+        assert c.kernel == L.APT_KERNEL_TC
+        assert c.bm == 128 and c.bn in (16, 64, 128, 256) and c.cluster_n in (1, 2, 4)
+        assert 1 <= c.split_k <= 8 and c.cluster_n * c.split_k <= 8
+        assert c.bn >= min(M, 128 if M > 64 else 64)
+        assert c.split_k == 1 or (c.bn <= 64 and c.cluster_n == 1)
 
 
 def test_selector_errors():
@@ -102,7 +105,7 @@ def test_gemm_argument_errors_before_launch():
     assert _gemm(16, 64, 256, 2, 2, W, A, kind=7) == E
     Wm = _fake_packed(64, 256, 2, addr=0x10004)                     # misaligned planes
     assert _gemm(16, 64, 256, 2, 2, Wm, A) == E
-    bad = L.AptConfig(L.APT_KERNEL_MMA_SPLITK, 2, 2, 16, 24, 256, 2, 1, 0, 1)  # bn 24 illegal
+    bad = L.AptConfig(L.APT_KERNEL_MMA_SPLITK, 2, 2, 32, 24, 256, 2, 4, 0, 1)  # bn 24 illegal
     assert _gemm(16, 64, 256, 2, 2, W, A, cfg=bad) == L.APT_ERR_UNSUPPORTED
     Wb, Ab = _fake_packed(64, 40000, 8), _fake_packed(16, 40000, 8)
     assert _gemm(16, 64, 40000, 8, 8, Wb, Ab) == L.APT_ERR_UNSUPPORTED
@@ -122,7 +125,7 @@ def test_pack_argument_errors():
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")
 def test_no_device_means_cuda_error_not_fallback():
     W, A = _fake_packed(64, 256, 2), _fake_packed(16, 256, 2)
-    assert _gemm(16, 64, 256, 2, 2, W, A) == L.APT_ERR_WORKSPACE   # no digit view and no workspace
+    assert _gemm(16, 64, 256, 2, 2, W, A) == L.APT_ERR_WORKSPACE   # tcgen05 path needs a digit view
     A.digits = 0x50000
     assert _gemm(16, 64, 256, 2, 2, W, A) == L.APT_ERR_CUDA
     out = L.AptPacked(0, 0, 0, 0, 0x10000, 0x20000)

@@ -132,25 +132,49 @@ def test_bound_rejected():
         P.gemm(W, A)
 
 
-@pytest.mark.parametrize("bn,split", [(8, 1), (16, 2), (8, 3), (16, 8), (8, 8)])
-def test_config_invariance_decode(bn, split):
-    """any legal configuration gives identical bits (decode kernel tiles / K split)."""
+@pytest.mark.parametrize("bn", [8, 16])
+def test_config_invariance_decode(bn):
+    """any legal configuration gives identical bits (decode kernel token tile)."""
     a = signed_codes(20, 4096, 4, seed=3)
     w = signed_codes(200, 4096, 3, seed=4)
     cfg = P.select_config(20, 200, 4096, 3, 4)
-    cfg.update(bn=bn, split_k=split)
+    cfg.update(bn=bn)
     _check_gemm(a, 4, w, 3, config=cfg)
 
 
-@pytest.mark.parametrize("bn,cn", [(128, 1), (128, 2), (128, 4), (256, 1), (256, 2)])
-def test_config_invariance_tc(bn, cn):
-    """S:336 for the tcgen05 kernel: token tile width and cluster multicast do not change the bits."""
-    a = signed_codes(300, 1000, 3, seed=5)
-    w = signed_codes(600, 1000, 5, seed=6)
-    cfg = P.select_config(300, 600, 1000, 5, 3)
-    stage = bn * 128 + 5 * 128 * 16
-    cfg.update(bn=bn, cluster_n=cn, stages=max(2, min(6, ((108 if bn <= 128 else 216) * 1024) // stage)))
-    _check_gemm(a, 3, w, 5, config=cfg)
+def test_decode_vs_tc_same_bits():
+    """The decode (mma.sync) and prefill (tcgen05) kernels agree bit for bit on one problem."""
+    a = signed_codes(40, 3000, 6, seed=8)
+    w = signed_codes(333, 3000, 5, seed=9)
+    A, W = _pack_both(a, 6, w, 5)
+    ct = P.select_config(40, 333, 3000, 5, 6)
+    cd = dict(ct, kernel=1, bm=32, bk=256, bn=16, split_k=4, stages=2, cluster_n=1)
+    assert ct["kernel"] == 2
+    y1 = P.gemm(W, A, config=cd).cpu().numpy()
+    y2 = P.gemm(W, A, config=ct).cpu().numpy()
+    assert np.array_equal(y1, y2)
+    assert np.array_equal(y1.astype(np.int64), O.gemm_signed(a, w))
+
+
+def _tc_stages(wb, bn):
+    cw = 8 if wb <= 4 else 4
+    slots = 6 if bn <= 64 else 2
+    v = ((108 if bn <= 128 else 216) * 1024 - slots * wb * 128 * cw * 4 - (128 * bn * 4 if bn <= 64 else 0)
+         - 4096) // (bn * 128)
+    return max(2, min(8, v))
+
+
+@pytest.mark.parametrize("bn,cn,split", [(128, 1, 1), (128, 2, 1), (128, 4, 1), (256, 1, 1), (256, 2, 1),
+                                         (16, 1, 1), (16, 1, 3), (16, 1, 8), (64, 1, 1), (64, 1, 5)])
+@pytest.mark.parametrize("wb,ab", [(5, 3), (2, 8)])
+def test_config_invariance_tc(bn, cn, split, wb, ab):
+    """S:336 for the tcgen05 kernel: token tile width, cluster multicast and cluster split-K do not
+    change the bits."""
+    a = signed_codes(300, 3000, ab, seed=5)
+    w = signed_codes(600, 3000, wb, seed=6)
+    cfg = P.select_config(300, 600, 3000, wb, ab)
+    cfg.update(bn=bn, cluster_n=cn, split_k=split, stages=_tc_stages(wb, bn))
+    _check_gemm(a, ab, w, wb, config=cfg)
 
 
 @pytest.mark.parametrize("m,pa,pw", [(1, 2, 1), (16, 4, 3), (300, 8, 2)])

@@ -50,7 +50,7 @@ for spec in sys.argv[1:]:
     torch.cuda.synchronize()
     buf = np.zeros(4096 * 8, dtype=np.uint64)
     P._lib.lib().apt_debug_mma_trace(ctypes.c_void_p(buf.ctypes.data), 4096 * 8)
-    ncta = min(4096, -(-n // 16) * -(-m // cfg["bn"]))
+    ncta = min(4096, -(-n // cfg["bm"]) * -(-m // cfg["bn"]))
     t = buf.reshape(4096, 8)[:ncta, :5].astype(np.int64)
     rel = t - t[:, 0].min()
     print(f"== {spec} cfg={cfg} ctas={ncta}   phases: {PH}")
