@@ -37,7 +37,7 @@ constexpr int kTcAStages = 4;    // TMEM A ring depth (32 columns each)
 #ifdef APT_TC_TRACE
 // per-stage clock64 timeline of CTA (APT_TC_TRACE_CTA, 0) for profiling builds only
 __device__ long long g_tc_trace[8][512];
-#define TRACE(slot, ks) do { if (blockIdx.x == APT_TC_TRACE_CTA && blockIdx.y == 0 && (ks) < 512) g_tc_trace[slot][(ks)] = clock64(); } while (0)
+#define TRACE(slot, ks) do { if (blockIdx.x == APT_TC_TRACE_CTA && blockIdx.y == 0 && blockIdx.z == 0 && (ks) < 512) g_tc_trace[slot][(ks)] = clock64(); } while (0)
 #else
 #define TRACE(slot, ks) do { } while (0)
 #endif
@@ -132,7 +132,7 @@ struct TcSmem {
   static constexpr int kBOff = 0;
   static constexpr int kWOff = STAGES * kBBytes;
   static constexpr int kRbOff = kWOff + kWSlots * kWBytes;       // split-K receive buffer [128][BN] i32
-  static constexpr int kEpOff = kRbOff + (BN <= 64 ? kTcBM * BN * 4 : 0);  // rw[128] ws[128] ra[BN] as[BN]
+  static constexpr int kEpOff = kRbOff + (BN <= 64 ? kTcBM * (BN + 8) * 4 : 0);  // rw[128] ws[128] ra[BN] as[BN]
   static constexpr int kBarOff = kEpOff + (2 * kTcBM + 2 * BN) * 4;
   static constexpr int kNumBars = 2 * STAGES + 2 * kWSlots + 2 * kTcAStages + 1;
   static constexpr int kTotal = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
         mbar_wait(empty(s), ph ^ 1);
         TRACE(0, j);
         mbar_expect_tx(full(s), L::kBBytes);
-        const uint32_t dstB = sB + s * L::kBBytes + crank * kRowsPerCta * kTcBK;
+        const uint32_t mc_rank = CN > 1 ? crank : 0u;  // cluster rank along x (multicast), not the K split
+        const uint32_t dstB = sB + s * L::kBBytes + mc_rank * kRowsPerCta * kTcBK;
         if (CN > 1)
           tma_load_2d_mc(dstB, &tm_b, full(s), ks * kTcBK, m0 + (int)crank * kRowsPerCta, kMask);
         else
@@ -393,6 +394,10 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t acc[16];
         tmem_ld16(tmem + lane_off + c0, acc);
+        if (nloc == 0) {  // an empty K range (more splits than weight chunks) contributes zero
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) acc[jj] = 0u;
+        }
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
           const int col = c0 + jj;
@@ -403,7 +408,10 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
         }
       }
     }
+    if (warp == 4 && lane == 0) TRACE(5, 3);
+    __syncwarp();  // reconverge the role-divergent warps: the cluster barrier is .aligned
     cluster_sync_all();
+    if (warp == 4 && lane == 0) TRACE(5, 4);
     if (warp >= 4) {
       const int r = (warp - 4) * 32 + lane;
       const int n = n0 + r;
@@ -421,6 +429,7 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
   if (warp == 4 && lane == 0) TRACE(5, 1);
   if (threadIdx.x == 0) TRACE(5, 2);
   tc_fence_before();
+  __syncwarp();  // reconverge the role-divergent warps before the .aligned barriers
   // no CTA may leave while cluster peers can still multicast into it or arrive on its barriers
   if (CN > 1) cluster_sync_all(); else __syncthreads();
   if (warp == 2) {
@@ -462,7 +471,7 @@ __host__ __device__ constexpr int tc_stages_ct(int wbits, int bn) {
   // at BN <= 128 (two CTAs per SM), ~216 KB at 256
   return tc_clamp(((bn <= 128 ? 108 : 216) * 1024 -
                    (bn <= 64 ? 6 : 2) * wbits * kTcBM * (wbits <= 4 ? 8 : 4) * 4 -
-                   (bn <= 64 ? kTcBM * bn * 4 : 0) - 4096) / (bn * kTcBK),
+                   (bn <= 64 ? kTcBM * (bn + 8) * 4 : 0) - 4096) / (bn * kTcBK),
                   2, 8);
 }
 

@@ -137,8 +137,8 @@ def test_config_invariance_decode(bn):
     """any legal configuration gives identical bits (decode kernel token tile)."""
     a = signed_codes(20, 4096, 4, seed=3)
     w = signed_codes(200, 4096, 3, seed=4)
-    cfg = P.select_config(20, 200, 4096, 3, 4)
-    cfg.update(bn=bn)
+    cfg = dict(P.select_config(20, 200, 4096, 3, 4), kernel=1, bm=32, bk=256, bn=bn, split_k=4, stages=2,
+               cluster_n=1)
     _check_gemm(a, 4, w, 3, config=cfg)
 
 
@@ -159,7 +159,7 @@ def test_decode_vs_tc_same_bits():
 def _tc_stages(wb, bn):
     cw = 8 if wb <= 4 else 4
     slots = 6 if bn <= 64 else 2
-    v = ((108 if bn <= 128 else 216) * 1024 - slots * wb * 128 * cw * 4 - (128 * bn * 4 if bn <= 64 else 0)
+    v = ((108 if bn <= 128 else 216) * 1024 - slots * wb * 128 * cw * 4 - (128 * (bn + 8) * 4 if bn <= 64 else 0)
          - 4096) // (bn * 128)
     return max(2, min(8, v))
 
