@@ -248,7 +248,7 @@ def main():
     barrier()
     e0.record()
     for (s, wb, n, k), c in W_codes.items():
-        W_packed[s][(wb, n, k)] = P.pack(c, wb)
+        W_packed[s][(wb, n, k)] = P.pack(c, wb, tiled=True)
     e1.record()
     barrier()
     wpack_ms = e0.elapsed_time(e1)

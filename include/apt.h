@@ -61,8 +61,17 @@ typedef enum {
                          x = (x' - 1) / 2.  int8 storage limits this encoding to n <= 7.     */
 } apt_encoding;
 
+typedef enum {
+  APT_PACK_ROWS = 0,  /* planes[i][r][w]: plane-major, row-major words (the canonical layout)            */
+  APT_PACK_TILED = 1  /* planes[i][r/128][w/8][r%128][w%8]: every 128-row x 256-element slab of a plane is
+                         4 KB contiguous, so the GEMM streams weight tiles with one bulk copy per plane
+                         (rows padded to a multiple of 128; pad-row words are unspecified and never
+                         reach a result).  Accepted for weights by the tcgen05 kernel.                     */
+} apt_pack_layout;
+
 /* The packed "unified matrix" (SPEC PackedPlanes S:35-41, with 32-bit words per P:252).
- *   planes  : uint32 [bits][rows][k_words], plane-major, one contiguous buffer.
+ *   planes  : uint32 [bits][rows][k_words] (layout APT_PACK_ROWS), plane-major, one contiguous buffer,
+ *             or the same words tile-major (APT_PACK_TILED, see apt_pack_layout).
  *             Plane i holds bit i of the bipolar pattern u = x + 2^(n-1) (the sign-bit-flipped
  *             two's-complement code).  Element c of a row is bit (c % 32) of word (c / 32),
  *             LSB first (reading Q5).  Pad elements c in [k, Kpad) hold the signed code 0,
@@ -85,17 +94,19 @@ typedef struct {
   uint32_t* planes;
   int32_t* row_sum;
   uint8_t* digits;
+  int32_t layout; /* apt_pack_layout of `planes`; set by the caller before apt_pack_bipolar */
 } apt_packed;
 
-/* Host.  Bytes of the `planes` buffer for a rows x k matrix of n-bit codes:
- * bits * rows * round_up(k,256)/32 * 4.  Returns 0 for invalid arguments. */
-APT_API size_t apt_packed_plane_bytes(int32_t rows, int32_t k, int32_t bits);
+/* Host.  Bytes of the `planes` buffer for a rows x k matrix of n-bit codes in `layout`:
+ * APT_PACK_ROWS bits * rows * round_up(k,256)/32 * 4; APT_PACK_TILED the same with rows rounded up to 128.
+ * Returns 0 for invalid arguments. */
+APT_API size_t apt_packed_plane_bytes(int32_t rows, int32_t k, int32_t bits, int32_t layout);
 
 /* Decomposition & reassembly (§4.1 Steps 1-3) on the device.
  *   codes       : int8 [rows][ld] row-major, element (r, c) at codes[r*ld + c], c < k.
  *   out         : host struct; out->planes (apt_packed_plane_bytes) and out->row_sum (rows int32)
- *                 must point to caller-allocated device buffers.  The call fills rows/k/k_words/bits
- *                 and writes both buffers (every word, including the padding).
+ *                 must point to caller-allocated device buffers and out->layout must be set.  The call
+ *                 fills rows/k/k_words/bits and writes both buffers (every word, including padding).
  *   range_error : nullable device int32.  If some code is outside the declared range, the kernel
  *                 stores 1 + (linear index r*k + c of one such code) there (first writer wins; the
  *                 caller zeroes it beforehand and reads it after its own synchronization).

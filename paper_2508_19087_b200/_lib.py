@@ -15,6 +15,7 @@ APT_ENC_SIGNED, APT_ENC_BIPOLAR = 0, 1
 APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
 APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
 APT_KERNEL_AUTO, APT_KERNEL_MMA_SPLITK, APT_KERNEL_TC = 0, 1, 2
+APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_select_config", "apt_gemm_workspace_bytes",
             "apt_gemm", "apt_status_string", "apt_abi_version"]
@@ -23,7 +24,7 @@ EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_select_config", "
 class AptPacked(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int32), ("k", ctypes.c_int32), ("k_words", ctypes.c_int32),
                 ("bits", ctypes.c_int32), ("planes", ctypes.c_void_p), ("row_sum", ctypes.c_void_p),
-                ("digits", ctypes.c_void_p)]
+                ("digits", ctypes.c_void_p), ("layout", ctypes.c_int32)]
 
 
 class AptScales(ctypes.Structure):
@@ -55,7 +56,7 @@ def lib():
             raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no fallback path exists)")
         L = ctypes.CDLL(LIB_PATH)
         L.apt_packed_plane_bytes.restype = ctypes.c_size_t
-        L.apt_packed_plane_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+        L.apt_packed_plane_bytes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
         L.apt_pack_bipolar.restype = ctypes.c_int
         L.apt_pack_bipolar.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                        ctypes.c_int32, ctypes.c_int, ctypes.POINTER(AptPacked), ctypes.c_void_p,

@@ -45,6 +45,7 @@ class Packed:
     k: int
     bits: int
     digits: torch.Tensor | None = None
+    tiled: bool = False  # planes in the tile-major layout (APT_PACK_TILED) the GEMM streams fastest
 
     @property
     def k_words(self) -> int:
@@ -52,34 +53,40 @@ class Packed:
 
     def struct(self) -> L.AptPacked:
         return L.AptPacked(self.rows, self.k, self.k_words, self.bits, self.planes.data_ptr(),
-                           self.row_sum.data_ptr(), self.digits.data_ptr() if self.digits is not None else None)
+                           self.row_sum.data_ptr(), self.digits.data_ptr() if self.digits is not None else None,
+                           L.APT_PACK_TILED if self.tiled else L.APT_PACK_ROWS)
 
     def narrow_rows(self, start: int, length: int) -> "Packed":
         """Rows [start, start+length) as a new packed matrix (copies the plane slices)."""
+        if self.tiled:
+            raise ValueError("narrow_rows needs the row-major plane layout")
         planes = self.planes[:, start:start + length].contiguous()
         digits = self.digits[start:start + length].contiguous() if self.digits is not None else None
         return Packed(planes, self.row_sum[start:start + length].contiguous(), length, self.k, self.bits, digits)
 
 
-def alloc_packed(rows: int, k: int, bits: int, device, digits: bool = False) -> Packed:
-    """Buffers for a packed operand; ``digits=True`` also allocates the u8 digit view (activations)."""
+def alloc_packed(rows: int, k: int, bits: int, device, digits: bool = False, tiled: bool = False) -> Packed:
+    """Buffers for a packed operand; ``digits=True`` also allocates the u8 digit view (activations),
+    ``tiled=True`` stores the planes tile-major (weights)."""
     kw = kpad(k) // 32
-    planes = torch.empty((bits, rows, kw), dtype=torch.int32, device=device)
+    prow = -(-rows // 128) * 128 if tiled else rows
+    planes = torch.empty((bits, prow, kw), dtype=torch.int32, device=device)
     row_sum = torch.empty((rows,), dtype=torch.int32, device=device)
     dig = torch.empty((rows, kw * 32), dtype=torch.uint8, device=device) if digits else None
-    return Packed(planes, row_sum, rows, k, bits, dig)
+    return Packed(planes, row_sum, rows, k, bits, dig, tiled)
 
 
 def pack(codes: torch.Tensor, bits: int, encoding: str = "signed", out: Packed | None = None,
-         range_error: torch.Tensor | None = None, stream=None, digits: bool = False) -> Packed:
+         range_error: torch.Tensor | None = None, stream=None, digits: bool = False, tiled: bool = False) -> Packed:
     """apt_pack_bipolar: int8 codes [rows, k] (row stride ``codes.stride(0)``) -> Packed.
-    ``digits=True`` (activations) also emits the kernel-order u8 digit view in the same pass."""
+    ``digits=True`` (activations) also emits the kernel-order u8 digit view in the same pass;
+    ``tiled=True`` (weights) writes the planes tile-major."""
     _require_cuda(codes, "codes")
     if codes.dtype != torch.int8 or codes.dim() != 2 or codes.stride(1) != 1:
         raise ValueError("codes must be a 2-D int8 tensor with unit stride along K")
     rows, k = codes.shape
     if out is None:
-        out = alloc_packed(rows, k, bits, codes.device, digits=digits)
+        out = alloc_packed(rows, k, bits, codes.device, digits=digits, tiled=tiled)
     st = out.struct()
     rc = L.lib().apt_pack_bipolar(codes.data_ptr(), rows, k, codes.stride(0), bits, _ENCODINGS[encoding],
                                   ctypes.byref(st), range_error.data_ptr() if range_error is not None else None,

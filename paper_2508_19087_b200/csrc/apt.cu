@@ -29,6 +29,7 @@ apt_status validate_packed(const apt_packed* P, int32_t rows, int32_t k, int32_t
   if (P->rows != rows || P->k != k || P->bits != bits) return APT_ERR_INVALID_ARGUMENT;
   if (P->k_words != kpad_of(k) / 32) return APT_ERR_INVALID_ARGUMENT;
   if (!aligned16(P->planes)) return APT_ERR_INVALID_ARGUMENT;
+  if (P->layout != APT_PACK_ROWS && P->layout != APT_PACK_TILED) return APT_ERR_INVALID_ARGUMENT;
   return APT_OK;
 }
 
@@ -52,6 +53,10 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
     if (c->split_k < 1 || c->split_k > 8) return APT_ERR_UNSUPPORTED;
     if (c->split_k > 1 && (c->bn > 64 || c->cluster_n != 1)) return APT_ERR_UNSUPPORTED;
     if (c->cluster_n > 1 && c->bn < 128) return APT_ERR_UNSUPPORTED;
+    if (c->bn == 16) {  // the up-front token slab holds at most 16 K steps per CTA
+      const int nch = (kw / 4 + 1) / 2;
+      if ((nch + c->split_k - 1) / c->split_k * 2 > 16) return APT_ERR_UNSUPPORTED;
+    }
     return APT_OK;
   }
   return APT_ERR_UNSUPPORTED;
@@ -74,9 +79,11 @@ const char* apt_status_string(apt_status s) {
   return "APT_ERR_UNKNOWN";
 }
 
-size_t apt_packed_plane_bytes(int32_t rows, int32_t k, int32_t bits) {
+size_t apt_packed_plane_bytes(int32_t rows, int32_t k, int32_t bits, int32_t layout) {
   if (rows <= 0 || k <= 0 || bits < 1 || bits > 8) return 0;
-  return (size_t)bits * (size_t)rows * (size_t)(kpad_of(k) / 32) * 4u;
+  if (layout != APT_PACK_ROWS && layout != APT_PACK_TILED) return 0;
+  const size_t prow = layout == APT_PACK_TILED ? (size_t)((rows + 127) / 128) * 128 : (size_t)rows;
+  return (size_t)bits * prow * (size_t)(kpad_of(k) / 32) * 4u;
 }
 
 apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k, int64_t ld, int32_t bits,
@@ -86,6 +93,7 @@ apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k, int64_
   if (enc != APT_ENC_SIGNED && enc != APT_ENC_BIPOLAR) return APT_ERR_INVALID_ARGUMENT;
   if (enc == APT_ENC_BIPOLAR && bits > 7) return APT_ERR_INVALID_ARGUMENT;
   if (!aligned16(out->planes)) return APT_ERR_INVALID_ARGUMENT;
+  if (out->layout != APT_PACK_ROWS && out->layout != APT_PACK_TILED) return APT_ERR_INVALID_ARGUMENT;
   out->rows = rows;
   out->k = k;
   out->k_words = (int32_t)(kpad_of(k) / 32);
@@ -98,7 +106,8 @@ apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k, int64_
   p.k_words = out->k_words;
   p.enc = (int32_t)enc;
   p.planes = out->planes;
-  p.plane_stride = (int64_t)rows * out->k_words;
+  p.tiled = out->layout == APT_PACK_TILED ? 1 : 0;
+  p.plane_stride = (int64_t)(p.tiled ? (rows + 127) / 128 * 128 : rows) * out->k_words;
   p.row_sum = out->row_sum;
   p.range_error = range_error;
   p.digits = out->digits;
@@ -123,20 +132,24 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
   if (M > 64) {
     // prefill: 128 weight rows x 128 tokens per CTA, two CTAs per SM, the token tile multicast to a
     // cluster of up to 4 weight tiles
-    out->bn = 128;
+    out->bn = wbits > 4 ? 256 : 128;  // wide weight chunks leave room for one 256-token CTA per SM
     out->split_k = 1;
-    out->cluster_n = ceil_div(N, 128) >= 4 ? 4 : ceil_div(N, 128) >= 2 ? 2 : 1;
+    out->cluster_n = ceil_div(N, 128) >= 4 && out->bn == 128 ? 4 : ceil_div(N, 128) >= 2 ? 2 : 1;
   } else {
     // decode: 16 (or 64) tokens per tile, K split over a cluster of up to 8 CTAs so that about two
     // CTAs per SM stream weights
     out->bn = M <= 16 ? 16 : 64;
     out->cluster_n = 1;
     const int64_t tiles = (int64_t)ceil_div(N, 128) * ceil_div(M, out->bn);
-    const int chunks = (kw / 4 + (wbits <= 4 ? 1 : 0)) / (wbits <= 4 ? 2 : 1);
+    const int chunks = (kw / 4 + 1) / 2;  // 256-element weight chunks
     int split = (int)((2 * kNumSMs + tiles / 2) / tiles);
     if (split > 8) split = 8;
     if (split > chunks) split = chunks;
     if (split < 1) split = 1;
+    if (out->bn == 16) {  // at most 16 K steps (8 chunks) per CTA, else the ring-buffered 64-token tile
+      while (split < 8 && (chunks + split - 1) / split > 8) ++split;
+      if ((chunks + split - 1) / split > 8) out->bn = 64;
+    }
     out->split_k = split;
   }
   out->stages = apt::tc_stages(wbits, out->bn);
@@ -196,6 +209,7 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   e.h_a = 1 << (abits - 1);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (c.kernel == APT_KERNEL_MMA_SPLITK) {
+    if (W->layout != APT_PACK_ROWS || A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
     apt::MmaArgs p;
     p.wp = W->planes;
     p.w_pstride = (int64_t)N * W->k_words;
@@ -210,6 +224,7 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   // the TC kernel reads the activation operand as kernel-order u8 digits: the packed view, or
   // expanded now into the workspace
   const uint8_t* adig = A->digits;
+  if (!adig && A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
   if (!adig) {
     cudaError_t err = apt::launch_expand_tokens(A->planes, (int64_t)M * A->k_words, M, A->k_words, abits,
                                                 reinterpret_cast<uint8_t*>(workspace), s);
@@ -219,7 +234,8 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   if (c.kernel == APT_KERNEL_TC) {
     apt::TcArgs p;
     p.wp = W->planes;
-    p.w_pstride = (int64_t)N * W->k_words;
+    p.w_tiled = W->layout == APT_PACK_TILED ? 1 : 0;
+    p.w_pstride = (int64_t)(p.w_tiled ? (N + 127) / 128 * 128 : N) * W->k_words;
     p.adig = adig;
     p.k_words = W->k_words;
     p.e = e;

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kDecThreads) gemm_mma_kernel(const __grid_cons
   const uint32_t ring = smem_u32(smem_raw + L.ring_off) + (uint32_t)(warp * D) * kSlab;
   const uint32_t bars = smem_u32(smem_raw + L.bar_off) + (uint32_t)(warp * D) * 8u;
 
+  pdl_launch_dependents();
   // 1. this warp's weight slabs in flight (TMA, one box = all planes of 16 rows x 256 elements)
   if (lane == 0) {
     for (int d = 0; d < D; ++d) mbar_init(bars + 8 * d, 1);
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(kDecThreads) gemm_mma_kernel(const __grid_cons
       tma_load_3d(ring + j * kSlab, &tm_w, bars + 8 * j, (it_b + j) * 8, n0 + rt * 16, 0);
     }
   }
+  pdl_wait();  // activations / outputs may belong to the previous kernel
   // 2. the CTA's token planes -> shared memory (cp.async, 16 B chunks), rows beyond M zero-filled
   {
     const int chunks_per_row = kw >> 2;
@@ -256,8 +258,7 @@ static cudaError_t launch_one(const CUtensorMap& tw, const MmaArgs& p, cudaStrea
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
   dim3 grid((p.e.N + kDecRows - 1) / kDecRows, (p.e.M + NT * 8 - 1) / (NT * 8));
-  kern<<<grid, kDecThreads, smem, stream>>>(tw, p);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(kDecThreads), smem, stream, dim3(1, 1, 1), tw, p);
 }
 
 template <int WB>

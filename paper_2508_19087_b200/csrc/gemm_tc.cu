@@ -100,6 +100,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 __global__ void __launch_bounds__(256) expand_tokens_kernel(const uint32_t* __restrict__ ap, int64_t a_pstride,
                                                             int32_t M, int32_t k_words, int32_t abits,
                                                             uint8_t* __restrict__ ws) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)M * k_words) return;
   uint32_t w[8];
@@ -115,8 +117,8 @@ __global__ void __launch_bounds__(256) expand_tokens_kernel(const uint32_t* __re
 cudaError_t launch_expand_tokens(const uint32_t* ap, int64_t a_pstride, int M, int k_words, int abits, uint8_t* out,
                                  cudaStream_t stream) {
   const int64_t total = (int64_t)M * k_words;
-  expand_tokens_kernel<<<(int)((total + 255) / 256), 256, 0, stream>>>(ap, a_pstride, M, k_words, abits, out);
-  return cudaGetLastError();
+  return launch_pdl(expand_tokens_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, stream, dim3(1, 1, 1),
+                    ap, a_pstride, M, k_words, abits, out);
 }
 
 // ------------------------------------------------------------------------------------ main kernel
@@ -124,13 +126,19 @@ template <int WB, int BN, int STAGES>
 struct TcSmem {
   // weight planes move in chunks of CW words (CW*32 K elements) per row and plane (32-byte TMA rows
   // for WB <= 4); decode-sized tiles keep more chunks in flight (HBM latency x bandwidth)
-  static constexpr int kCW = WB <= 4 ? 8 : 4;
+  static constexpr int kCW = 8;
   static constexpr int kKpc = kCW / 4;                  // 128-element K steps per weight chunk
-  static constexpr int kWSlots = BN <= 64 ? 6 : 2;
+  // BN == 16 (decode): the CTA's whole token slab (<= kBAllSteps K steps) is loaded once up front,
+  // so the TMA queue in steady state carries only the weight stream; the rest of ~113 KB (two
+  // CTAs per SM) goes to weight chunks in flight
+  static constexpr bool kBAll = BN == 16;
+  static constexpr int kBAllSteps = 16;
+  static constexpr int kWSlots = kBAll ? ((65536 / (WB * kTcBM * 8 * 4)) > 8 ? 8 : (65536 / (WB * kTcBM * 8 * 4)) < 2 ? 2 : (65536 / (WB * kTcBM * 8 * 4)))
+                                       : BN <= 64 ? (WB <= 4 ? 6 : 3) : 2;
   static constexpr int kBBytes = BN * kTcBK;            // token digits per K step
   static constexpr int kWBytes = WB * kTcBM * kCW * 4;  // weight planes per chunk
   static constexpr int kBOff = 0;
-  static constexpr int kWOff = STAGES * kBBytes;
+  static constexpr int kWOff = (kBAll ? kBAllSteps : STAGES) * kBBytes;
   static constexpr int kRbOff = kWOff + kWSlots * kWBytes;       // split-K receive buffer [128][BN] i32
   static constexpr int kEpOff = kRbOff + (BN <= 64 ? kTcBM * (BN + 8) * 4 : 0);  // rw[128] ws[128] ra[BN] as[BN]
   static constexpr int kBarOff = kEpOff + (2 * kTcBM + 2 * BN) * 4;
@@ -152,6 +160,21 @@ __device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+template <int NC>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[NC]);
+template <>
+__device__ __forceinline__ void tmem_ld<8>(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]);
+template <>
+__device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t (&r)[16]) { tmem_ld16(taddr, r); }
+template <>
+__device__ __forceinline__ void tmem_ld<32>(uint32_t taddr, uint32_t (&r)[32]) { tmem_ld32(taddr, r); }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -167,7 +190,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // gridDim.z = S > 1 (with CN = 1): the K steps are split over a (1, 1, S) cluster and the S partial
 // accumulator tiles are reduced through distributed shared memory (decode-sized token counts).
 template <int WB, int BN, int STAGES, int CN>
-__global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w,
+__global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w,
                                                          const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
   using L = TcSmem<WB, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -206,6 +229,7 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
   const int kb = min(nk, (int)((blockIdx.z * nch) / S) * L::kKpc);
   const int ke = min(nk, (int)(((blockIdx.z + 1) * nch) / S) * L::kKpc);
   const int nloc = ke - kb;
+  pdl_launch_dependents();
   if (threadIdx.x == 0) TRACE(6, 0);
 
   if (threadIdx.x == 0) {
@@ -215,7 +239,7 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
     }
     for (int c = 0; c < L::kWSlots; ++c) {
       mbar_init(wfull(c), 1);
-      mbar_init(wempty(c), 4);      // the 4 converter warps
+      mbar_init(wempty(c), 8);      // the 8 converter warps (each reads one K step of the chunk)
     }
     for (int a = 0; a < kTcAStages; ++a) {
       mbar_init(a_full(a), 4);
@@ -243,14 +267,37 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      auto issue_w = [&](int c) {  // weight chunk c: all planes of 128 rows x kCW words
+        const int ks = kb + c * L::kKpc;
+        mbar_wait(wempty(c % L::kWSlots), ((c / L::kWSlots) & 1) ^ 1);
+        mbar_expect_tx(wfull(c % L::kWSlots), L::kWBytes);
+        const uint32_t dstW = sW + (c % L::kWSlots) * L::kWBytes;
+        if (p.w_tiled) {
+          // tile-major planes: each plane's 128-row x 8-word slab is 4 KB contiguous
+          const uint32_t* src = p.wp + ((int64_t)(n0 >> 7) * (p.k_words >> 3) + (ks >> 1)) * 1024;
+#pragma unroll
+          for (int i = 0; i < WB; ++i)
+            bulk_load(dstW + i * 4096, src + (int64_t)i * p.w_pstride, 4096, wfull(c % L::kWSlots));
+        } else {
+          tma_load_3d(dstW, &tm_w, wfull(c % L::kWSlots), ks * 4, n0, 0);
+        }
+      };
+      // weights never depend on the previous kernel: the first ring's worth of chunks is requested
+      // before waiting for it (programmatic dependent launch)
+      const int n_pre = min(L::kWSlots, (nloc + L::kKpc - 1) / L::kKpc);
+      for (int c = 0; c < n_pre; ++c) issue_w(c);
+      pdl_wait();
+      if constexpr (L::kBAll) {
+        // the whole token slab of this CTA's K range, one barrier
+        mbar_expect_tx(full(0), (uint32_t)(nloc * L::kBBytes));
+        for (int j = 0; j < nloc; ++j) tma_load_2d(sB + j * L::kBBytes, &tm_b, full(0), (kb + j) * kTcBK, m0);
+      }
       for (int j = 0; j < nloc; ++j) {
         const int ks = kb + j;
-        if (j % L::kKpc == 0) {  // next weight chunk: all planes of 128 rows x kCW words, one box
-          const int c = j / L::kKpc;
-          mbar_wait(wempty(c % L::kWSlots), ((c / L::kWSlots) & 1) ^ 1);
-          mbar_expect_tx(wfull(c % L::kWSlots), L::kWBytes);
-          tma_load_3d(sW + (c % L::kWSlots) * L::kWBytes, &tm_w, wfull(c % L::kWSlots), ks * 4, n0, 0);
+        if (j % L::kKpc == 0 && j / L::kKpc >= n_pre) {  // next weight chunk
+          issue_w(j / L::kKpc);
         }
+        if constexpr (L::kBAll) continue;
         const int s = j % STAGES;
         const uint32_t ph = (j / STAGES) & 1;
         mbar_wait(empty(s), ph ^ 1);
@@ -271,11 +318,11 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
                                  | ((uint32_t)(BN >> 3) << 17)   // N
                                  | ((uint32_t)(kTcBM >> 4) << 24);  // M ; A, B = u8, K-major
       for (int j = 0; j < nloc; ++j) {
-        const int s = j % STAGES;
+        const int s = L::kBAll ? j : j % STAGES;
         const uint32_t ph = (j / STAGES) & 1;
         const int a = j % kTcAStages;
         const uint32_t pa = (j / kTcAStages) & 1;
-        mbar_wait(full(s), ph);
+        if (!L::kBAll || j == 0) mbar_wait(full(L::kBAll ? 0 : s), L::kBAll ? 0u : ph);
         TRACE(1, j);
         mbar_wait(a_full(a), pa);
         TRACE(2, j);
@@ -286,45 +333,45 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
           // advance 32 K bytes inside the 128-byte swizzle atom: +2 in the (addr >> 4) field
           tc_mma_i8(tmem, tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk), idesc, (j | kk) != 0);
         }
-        if (CN > 1) tc_commit_mc(empty(s), kMask); else tc_commit(empty(s));
+        if (!L::kBAll) {
+          if (CN > 1) tc_commit_mc(empty(s), kMask); else tc_commit(empty(s));
+        }
         tc_commit(a_empty(a));
       }
       tc_commit(acc_full);
     }
   } else if (warp < 4) {
     // ------------------------------------------------------------ epilogue operands (warps 2, 3)
-    for (int i = threadIdx.x - 64; i < kTcBM + BN; i += 64) {
-      if (i < kTcBM) {
-        const int n = min(n0 + i, p.e.N - 1);
-        ep_rw[i] = __ldg(p.e.w_rowsum + n);
-        ep_ws[i] = p.e.kind == 2 ? __ldg(p.e.w_scale + n) : 0.f;
-      } else {
-        const int m = min(m0 + i - kTcBM, p.e.M - 1);
-        ep_ra[i - kTcBM] = __ldg(p.e.a_rowsum + m);
-        ep_as[i - kTcBM] = (p.e.kind == 2 && p.e.a_scale) ? __ldg(p.e.a_scale + m) : 1.f;
-      }
+    for (int i = threadIdx.x - 64; i < kTcBM; i += 64) {  // weight side: immutable
+      const int n = min(n0 + i, p.e.N - 1);
+      ep_rw[i] = __ldg(p.e.w_rowsum + n);
+      ep_ws[i] = p.e.kind == 2 ? __ldg(p.e.w_scale + n) : 0.f;
     }
-    asm volatile("bar.arrive 1, 192;" ::: "memory");
+    pdl_wait();  // token side: written by the previous kernel (the activation pack)
+    for (int i = threadIdx.x - 64; i < BN; i += 64) {
+      const int m = min(m0 + i, p.e.M - 1);
+      ep_ra[i] = __ldg(p.e.a_rowsum + m);
+      ep_as[i] = (p.e.kind == 2 && p.e.a_scale) ? __ldg(p.e.a_scale + m) : 1.f;
+    }
+    asm volatile("bar.arrive 1, 320;" ::: "memory");
   } else {
-    // ------------------------------------------------------------ converters (warps 4..7)
-    const int sub = warp - 4;            // TMEM sub-partition (lanes 32*sub ..)
-    const int r = sub * 32 + lane;       // row within the tile
+    // ------------------------------------------------------------ converters (warps 4..11)
+    // two warps per TMEM sub-partition: parity `par` converts the K steps j with j % 2 == par, so
+    // one warp's shared-memory / rebuild / tcgen05.st latency overlaps the other's
+    const int cw = warp - 4, sub = cw & 3, par = cw >> 2;
+    const int r = sub * 32 + lane;       // row within the tile (= TMEM lane)
     const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
-    for (int j = 0; j < nloc; ++j) {
-      const int c = j / L::kKpc, q = j % L::kKpc;
-      if (q == 0) {
-        mbar_wait(wfull(c % L::kWSlots), (c / L::kWSlots) & 1);
-        if (lane == 0 && sub == 0) TRACE(3, j);
-      }
+    for (int j = par; j < nloc; j += 2) {
+      const int c = j / L::kKpc, q = j % L::kKpc;  // kKpc == 2: each parity reads one step per chunk
+      mbar_wait(wfull(c % L::kWSlots), (c / L::kWSlots) & 1);
+      if (lane == 0 && cw == 0) TRACE(3, j);
       uint4 v[WB];
       const uint8_t* wsm = gbase + L::kWOff + (c % L::kWSlots) * L::kWBytes;
 #pragma unroll
       for (int i = 0; i < WB; ++i)
         v[i] = *reinterpret_cast<const uint4*>(wsm + ((i * kTcBM + r) * L::kCW + 4 * q) * 4);
-      if (q == L::kKpc - 1 || j == nloc - 1) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(wempty(c % L::kWSlots));
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(wempty(c % L::kWSlots));
       uint32_t d[32];
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
@@ -344,62 +391,47 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full(a));
-      if (lane == 0 && sub == 0) TRACE(4, j);
+      if (lane == 0 && cw == 0) TRACE(4, j);
     }
     // ------------------------------------------------------------ epilogue
-    asm volatile("bar.sync 1, 192;" ::: "memory");   // epilogue operands are in shared memory
+    // warp (sub, par) owns rows 32*sub.. and the token columns [par*BN/2, (par+1)*BN/2)
+    asm volatile("bar.sync 1, 320;" ::: "memory");   // epilogue operands are in shared memory
     mbar_wait(acc_full, 0);
-    if (lane == 0 && sub == 0) TRACE(5, 0);
+    if (lane == 0 && cw == 0) TRACE(5, 0);
     tc_fence_after();
+    constexpr int kHalf = BN / 2;
+    constexpr int kChunk = kHalf < 32 ? kHalf : 32;
     const int n = n0 + r;
     const int32_t rw = ep_rw[r];
     const float wsc = ep_ws[r];
     if (S == 1) {
-      if constexpr (BN % 32 == 0) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          uint32_t acc[32];
-          tmem_ld32(tmem + lane_off + c0, acc);
-          if (n < p.e.N) {
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              const int m = m0 + c0 + jj;
-              if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[jj], ep_ra[c0 + jj], rw, wsc, ep_as[c0 + jj]);
-            }
-          }
-        }
-      } else {
-        uint32_t acc[16];
-        tmem_ld16(tmem + lane_off, acc);
+      for (int c0 = par * kHalf; c0 < (par + 1) * kHalf; c0 += kChunk) {
+        uint32_t acc[kChunk];
+        tmem_ld<kChunk>(tmem + lane_off + c0, acc);
         if (n < p.e.N) {
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            const int m = m0 + jj;
-            if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[jj], ep_ra[jj], rw, wsc, ep_as[jj]);
+          for (int jj = 0; jj < kChunk; ++jj) {
+            const int m = m0 + c0 + jj;
+            if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[jj], ep_ra[c0 + jj], rw, wsc, ep_as[c0 + jj]);
           }
         }
       }
-    }
-  }
-  if (BN <= 64 && S > 1) {
-    // ------------------------------------------------------------ split-K reduction over the cluster
-    // converter/epilogue warps push their row's partial of token column c to rank c % S; one cluster
-    // barrier; every rank sums its columns and stores them
-    const int slots = (BN + S - 1) / S;
-    if (warp >= 4) {
-      const int r = (warp - 4) * 32 + lane;
-      const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    } else if constexpr (BN <= 64) {
+      // ---------------------------------------------------------- split-K: push partials over DSMEM
+      // the partial of token column col goes to cluster rank col % S, slot col / S
+      const int slots = (BN + S - 1) / S;
       const uint32_t rb_local = smem_u32(rbuf);
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t acc[16];
-        tmem_ld16(tmem + lane_off + c0, acc);
+#pragma unroll 1
+      for (int c0 = par * kHalf; c0 < (par + 1) * kHalf; c0 += kChunk) {
+        uint32_t acc[kChunk];
+        tmem_ld<kChunk>(tmem + lane_off + c0, acc);
         if (nloc == 0) {  // an empty K range (more splits than weight chunks) contributes zero
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) acc[jj] = 0u;
+          for (int jj = 0; jj < kChunk; ++jj) acc[jj] = 0u;
         }
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
+        for (int jj = 0; jj < kChunk; ++jj) {
           const int col = c0 + jj;
           const uint32_t off = (uint32_t)((((int)crank * kTcBM + r) * slots + col / S) * 4);
           uint32_t remote;
@@ -408,14 +440,19 @@ __global__ void __launch_bounds__(256, BN <= 128 ? 2 : 1) gemm_tc_kernel(const _
         }
       }
     }
+  }
+  if (BN <= 64 && S > 1) {
+    // every rank sums the partials of its token columns (col = rank + S * slot) and stores them
+    const int slots = (BN + S - 1) / S;
     if (warp == 4 && lane == 0) TRACE(5, 3);
     __syncwarp();  // reconverge the role-divergent warps: the cluster barrier is .aligned
     cluster_sync_all();
     if (warp == 4 && lane == 0) TRACE(5, 4);
     if (warp >= 4) {
-      const int r = (warp - 4) * 32 + lane;
+      const int cw = warp - 4, sub = cw & 3, par = cw >> 2;
+      const int r = sub * 32 + lane;
       const int n = n0 + r;
-      for (int sl = 0; sl < slots; ++sl) {
+      for (int sl = par; sl < slots; sl += 2) {
         const int col = (int)crank + S * sl;
         const int m = m0 + col;
         if (col < BN && m < p.e.M && n < p.e.N) {
@@ -470,7 +507,7 @@ __host__ __device__ constexpr int tc_stages_ct(int wbits, int bn) {
   // token-tile ring as deep as shared memory allows next to the weight-chunk ring: ~108 KB per CTA
   // at BN <= 128 (two CTAs per SM), ~216 KB at 256
   return tc_clamp(((bn <= 128 ? 108 : 216) * 1024 -
-                   (bn <= 64 ? 6 : 2) * wbits * kTcBM * (wbits <= 4 ? 8 : 4) * 4 -
+                   (bn <= 64 ? (wbits <= 4 ? 6 : 3) : 2) * wbits * kTcBM * 8 * 4 -
                    (bn <= 64 ? kTcBM * (bn + 8) * 4 : 0) - 4096) / (bn * kTcBK),
                   2, 8);
 }
@@ -483,23 +520,13 @@ template <int WB, int BN, int ST, int CN>
 static cudaError_t launch_tc4(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int split,
                               cudaStream_t stream) {
   using L = TcSmem<WB, BN, ST>;
+  static_assert(L::kTotal <= 227 * 1024, "shared memory budget");
   auto kern = gemm_tc_kernel<WB, BN, ST, CN>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
   if (err != cudaSuccess) return err;
   const int gx = ((p.e.N + kTcBM - 1) / kTcBM + CN - 1) / CN * CN;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(gx, (p.e.M + BN - 1) / BN, split);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = L::kTotal;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CN;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = split;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tw, tb, p);
+  return launch_pdl(kern, dim3(gx, (p.e.M + BN - 1) / BN, split), dim3(384), L::kTotal, stream, dim3(CN, 1, split),
+                    tw, tb, p);
 }
 
 template <int WB, int BN>
@@ -532,7 +559,7 @@ cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, in
   PFN_encodeTiled_t enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tw, tb;
-  const int cw = wbits <= 4 ? 8 : 4;
+  const int cw = 8;
   if (!make_plane_map(&tw, p.wp, p.k_words, p.e.N, wbits, cw, kTcBM)) return cudaErrorInvalidValue;
   {
     const cuuint64_t kp = (cuuint64_t)p.k_words * 32;

@@ -16,6 +16,7 @@ struct PackArgs {
   int32_t* row_sum;
   int32_t* range_error;
   uint8_t* digits;       // optional [rows][Kpad] kernel-order u8 digits
+  int32_t tiled;         // planes tile-major (APT_PACK_TILED)
 };
 cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream);
 
@@ -39,8 +40,9 @@ cudaError_t launch_expand_tokens(const uint32_t* ap, int64_t a_pstride, int M, i
 
 namespace apt {
 struct TcArgs {
-  const uint32_t* wp;      // weight planes [wbits][N][k_words]
-  int64_t w_pstride;       // N * k_words
+  const uint32_t* wp;      // weight planes [wbits][N][k_words] or tile-major (w_tiled)
+  int64_t w_pstride;       // words per plane
+  int32_t w_tiled;
   const uint8_t* adig;     // activation digits [M][Kpad], kernel K order (TMA source)
   int32_t k_words;
   EpilogueArgs e;

@@ -1,6 +1,6 @@
 // pack.cu — INT -> bipolar-INT bit-plane packing on the device (§4.1 Steps 1-3).
 //
-// One CTA per matrix row; each thread owns one 32-bit output word position (32 consecutive K
+// One CTA per matrix row, one thread per 32-bit output word position (32 consecutive K
 // elements) at a time and loads those 32 codes as two 16-byte vectors (a warp reads 1 KB of
 // contiguous codes).  Per 4-byte group of codes:
 //   signed -> offset bits   u = x + 2^(n-1) mod 2^n, i.e. the sign-bit flip of P:202, done
@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.h"
+#include "sync.cuh"
 
 namespace apt {
 
@@ -44,7 +45,9 @@ __device__ __forceinline__ uint32_t from_offset4(uint32_t u) {
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(128) pack_kernel(PackArgs p) {
+__global__ void __launch_bounds__(1024) pack_kernel(PackArgs p) {
+  pdl_launch_dependents();  // the next kernel (a GEMM) may start streaming its weights now
+  pdl_wait();               // our codes / output buffers may still be in use by the previous kernel
   const int r = blockIdx.x;
   const int8_t* row = p.codes + (int64_t)r * p.ld;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0);
@@ -110,7 +113,8 @@ __global__ void __launch_bounds__(128) pack_kernel(PackArgs p) {
       }
     }
     // planes: bit i of every element, element c -> bit c % 32 (LSB first)
-    uint32_t* dst = p.planes + (int64_t)r * p.k_words + w;
+    uint32_t* dst = p.tiled ? p.planes + ((int64_t)(r >> 7) * (p.k_words >> 3) + (w >> 3)) * 1024 + (r & 127) * 8 + (w & 7)
+                            : p.planes + (int64_t)r * p.k_words + w;
     uint32_t pw[BITS];
 #pragma unroll
     for (int i = 0; i < BITS; ++i) {
@@ -133,25 +137,34 @@ __global__ void __launch_bounds__(128) pack_kernel(PackArgs p) {
     }
   }
   // CTA reduction of the row sum (pads contribute 0)
-  __shared__ int red[4];
+  __shared__ int red[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
   __syncthreads();
-  if (threadIdx.x == 0) p.row_sum[r] = red[0] + red[1] + red[2] + red[3];
+  if (threadIdx.x < 32) {
+    int v = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) p.row_sum[r] = v;
+  }
 }
 
 cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream) {
-  dim3 grid(p.rows), block(128);
+  // one CTA per row with (up to) one thread per 32-element word: a single latency round for K <= 32768
+  int threads = ((p.k_words + 31) / 32) * 32;
+  if (threads > 1024) threads = 1024;
+  if (threads < 32) threads = 32;
+  dim3 grid(p.rows), block(threads);
   switch (bits) {
-    case 1: pack_kernel<1><<<grid, block, 0, stream>>>(p); break;
-    case 2: pack_kernel<2><<<grid, block, 0, stream>>>(p); break;
-    case 3: pack_kernel<3><<<grid, block, 0, stream>>>(p); break;
-    case 4: pack_kernel<4><<<grid, block, 0, stream>>>(p); break;
-    case 5: pack_kernel<5><<<grid, block, 0, stream>>>(p); break;
-    case 6: pack_kernel<6><<<grid, block, 0, stream>>>(p); break;
-    case 7: pack_kernel<7><<<grid, block, 0, stream>>>(p); break;
-    default: pack_kernel<8><<<grid, block, 0, stream>>>(p); break;
+    case 1: return launch_pdl(pack_kernel<1>, grid, block, 0, stream, dim3(1, 1, 1), p);
+    case 2: return launch_pdl(pack_kernel<2>, grid, block, 0, stream, dim3(1, 1, 1), p);
+    case 3: return launch_pdl(pack_kernel<3>, grid, block, 0, stream, dim3(1, 1, 1), p);
+    case 4: return launch_pdl(pack_kernel<4>, grid, block, 0, stream, dim3(1, 1, 1), p);
+    case 5: return launch_pdl(pack_kernel<5>, grid, block, 0, stream, dim3(1, 1, 1), p);
+    case 6: return launch_pdl(pack_kernel<6>, grid, block, 0, stream, dim3(1, 1, 1), p);
+    case 7: return launch_pdl(pack_kernel<7>, grid, block, 0, stream, dim3(1, 1, 1), p);
+    default: return launch_pdl(pack_kernel<8>, grid, block, 0, stream, dim3(1, 1, 1), p);
   }
   return cudaGetLastError();
 }

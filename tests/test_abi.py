@@ -35,11 +35,15 @@ def test_status_strings():
 
 def test_plane_bytes():
     lib = L.lib()
-    assert lib.apt_packed_plane_bytes(4096, 4096, 2) == 2 * 4096 * 128 * 4
-    assert lib.apt_packed_plane_bytes(3, 1, 8) == 8 * 3 * 8 * 4
-    assert lib.apt_packed_plane_bytes(3, 257, 3) == 3 * 3 * 16 * 4
-    assert lib.apt_packed_plane_bytes(0, 5, 2) == 0
-    assert lib.apt_packed_plane_bytes(5, 5, 9) == 0
+    R, T = L.APT_PACK_ROWS, L.APT_PACK_TILED
+    assert lib.apt_packed_plane_bytes(4096, 4096, 2, R) == 2 * 4096 * 128 * 4
+    assert lib.apt_packed_plane_bytes(3, 1, 8, R) == 8 * 3 * 8 * 4
+    assert lib.apt_packed_plane_bytes(3, 257, 3, R) == 3 * 3 * 16 * 4
+    assert lib.apt_packed_plane_bytes(3, 257, 3, T) == 3 * 128 * 16 * 4
+    assert lib.apt_packed_plane_bytes(11008, 4096, 4, T) == 4 * 11008 * 128 * 4
+    assert lib.apt_packed_plane_bytes(0, 5, 2, R) == 0
+    assert lib.apt_packed_plane_bytes(5, 5, 9, R) == 0
+    assert lib.apt_packed_plane_bytes(5, 5, 2, 7) == 0
 
 
 def _select(M, N, K, wb, ab):
@@ -78,7 +82,7 @@ def test_selector_errors():
 
 
 def _fake_packed(rows, k, bits, addr=0x10000):
-    return L.AptPacked(rows, k, -(-k // 256) * 8, bits, addr, addr + 0x1000000)
+    return L.AptPacked(rows, k, -(-k // 256) * 8, bits, addr, addr + 0x1000000, None, L.APT_PACK_ROWS)
 
 
 def _gemm(M, N, K, wb, ab, W, A, kind=0, layout=0, out=0x30000, ldo=None, scales=None, cfg=None):
@@ -113,13 +117,15 @@ def test_gemm_argument_errors_before_launch():
 
 def test_pack_argument_errors():
     lib = L.lib()
-    out = L.AptPacked(0, 0, 0, 0, 0x10000, 0x20000)
+    out = L.AptPacked(0, 0, 0, 0, 0x10000, 0x20000, None, L.APT_PACK_ROWS)
     E = L.APT_ERR_INVALID_ARGUMENT
     assert lib.apt_pack_bipolar(None, 4, 4, 4, 2, 0, ctypes.byref(out), None, None) == E
     assert lib.apt_pack_bipolar(0x1000, 4, 4, 3, 2, 0, ctypes.byref(out), None, None) == E   # ld < k
     assert lib.apt_pack_bipolar(0x1000, 4, 4, 4, 9, 0, ctypes.byref(out), None, None) == E
     assert lib.apt_pack_bipolar(0x1000, 4, 4, 4, 8, 1, ctypes.byref(out), None, None) == E   # bipolar n=8
     assert lib.apt_pack_bipolar(0x1000, 0, 4, 4, 2, 0, ctypes.byref(out), None, None) == E
+    out.layout = 5
+    assert lib.apt_pack_bipolar(0x1000, 4, 4, 4, 2, 0, ctypes.byref(out), None, None) == E
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")
@@ -128,7 +134,7 @@ def test_no_device_means_cuda_error_not_fallback():
     assert _gemm(16, 64, 256, 2, 2, W, A) == L.APT_ERR_WORKSPACE   # tcgen05 path needs a digit view
     A.digits = 0x50000
     assert _gemm(16, 64, 256, 2, 2, W, A) == L.APT_ERR_CUDA
-    out = L.AptPacked(0, 0, 0, 0, 0x10000, 0x20000)
+    out = L.AptPacked(0, 0, 0, 0, 0x10000, 0x20000, None, L.APT_PACK_ROWS)
     assert L.lib().apt_pack_bipolar(0x1000, 4, 4, 4, 2, 0, ctypes.byref(out), None, None) == L.APT_ERR_CUDA
 
 

@@ -22,10 +22,19 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
 
 
-def _pack_both(a_codes, abits, w_codes, wbits):
+def _pack_both(a_codes, abits, w_codes, wbits, tiled=True):
     A = P.pack(_dev(a_codes), abits)
-    W = P.pack(_dev(w_codes), wbits)
+    W = P.pack(_dev(w_codes), wbits, tiled=tiled)
     return A, W
+
+
+def _tiled_from_rows(planes):
+    """Tile-major view of canonical planes [bits][rows][kw] (APT_PACK_TILED, pad rows ignored)."""
+    bits, rows, kw = planes.shape
+    rb = -(-rows // 128)
+    full = np.zeros((bits, rb * 128, kw), dtype=planes.dtype)
+    full[:, :rows] = planes
+    return full.reshape(bits, rb, 128, kw // 8, 8).transpose(0, 1, 3, 2, 4)
 
 
 # ----------------------------------------------------------------------------- pack (T6)
@@ -38,6 +47,22 @@ def test_pack_matches_oracle(bits, rows, k):
     planes, rs = O.pack_planes(codes, bits)
     torch.cuda.synchronize()
     assert np.array_equal(got.planes.cpu().numpy().view(np.uint32), planes)
+    assert np.array_equal(got.row_sum.cpu().numpy().astype(np.int64), rs)
+
+
+@pytest.mark.parametrize("bits", [1, 3, 4, 8])
+@pytest.mark.parametrize("rows,k", [(1, 1), (130, 700), (256, 4096)])
+def test_pack_tiled_layout(bits, rows, k):
+    """APT_PACK_TILED holds exactly the canonical words, tile-major (pad rows excluded)."""
+    codes = signed_codes(rows, k, bits, seed=7 * bits + rows)
+    got = P.pack(_dev(codes), bits, tiled=True)
+    planes, rs = O.pack_planes(codes, bits)
+    g = got.planes.cpu().numpy().view(np.uint32)
+    rb = -(-rows // 128)
+    g = g.reshape(bits, rb, planes.shape[2] // 8, 128, 8)
+    want = _tiled_from_rows(planes)
+    for r in range(rows):
+        assert np.array_equal(g[:, r // 128, :, r % 128, :], want[:, r // 128, :, r % 128, :])
     assert np.array_equal(got.row_sum.cpu().numpy().astype(np.int64), rs)
 
 
@@ -74,8 +99,8 @@ def test_pack_range_error_flag():
 
 # ----------------------------------------------------------------------------- GEMM (T7)
 
-def _check_gemm(a, abits, w, wbits, config=None, layouts=("row",)):
-    A, W = _pack_both(a, abits, w, wbits)
+def _check_gemm(a, abits, w, wbits, config=None, layouts=("row",), tiled=True):
+    A, W = _pack_both(a, abits, w, wbits, tiled=tiled)
     y = O.gemm_signed(a, w)
     yb = O.gemm_bipolar(a, abits, w, wbits) if a.shape[1] * a.shape[0] * w.shape[0] < 3e6 else \
         4 * y + 2 * a.astype(np.int64).sum(1)[:, None] + 2 * w.astype(np.int64).sum(1)[None, :] + a.shape[1]
@@ -90,10 +115,10 @@ def _check_gemm(a, abits, w, wbits, config=None, layouts=("row",)):
 
 @pytest.mark.parametrize("seed", range(20))
 def test_config1_w2a2(seed):
-    """BASELINE configs[0]: W2A2, M=16, N=K=256."""
+    """BASELINE configs[0]: W2A2, M=16, N=K=256 (tiled and row-major weight planes)."""
     a = signed_codes(16, 256, 2, seed=config_seed(0, 2, 2, seed))
     w = signed_codes(256, 256, 2, seed=config_seed(0, 2, 2, seed) + 7)
-    _check_gemm(a, 2, w, 2, layouts=("row", "col"))
+    _check_gemm(a, 2, w, 2, layouts=("row", "col"), tiled=bool(seed % 2))
 
 
 def test_random_set():
@@ -139,14 +164,14 @@ def test_config_invariance_decode(bn):
     w = signed_codes(200, 4096, 3, seed=4)
     cfg = dict(P.select_config(20, 200, 4096, 3, 4), kernel=1, bm=32, bk=256, bn=bn, split_k=4, stages=2,
                cluster_n=1)
-    _check_gemm(a, 4, w, 3, config=cfg)
+    _check_gemm(a, 4, w, 3, config=cfg, tiled=False)
 
 
 def test_decode_vs_tc_same_bits():
     """The decode (mma.sync) and prefill (tcgen05) kernels agree bit for bit on one problem."""
     a = signed_codes(40, 3000, 6, seed=8)
     w = signed_codes(333, 3000, 5, seed=9)
-    A, W = _pack_both(a, 6, w, 5)
+    A, W = _pack_both(a, 6, w, 5, tiled=False)
     ct = P.select_config(40, 333, 3000, 5, 6)
     cd = dict(ct, kernel=1, bm=32, bk=256, bn=16, split_k=4, stages=2, cluster_n=1)
     assert ct["kernel"] == 2
@@ -157,15 +182,15 @@ def test_decode_vs_tc_same_bits():
 
 
 def _tc_stages(wb, bn):
-    cw = 8 if wb <= 4 else 4
-    slots = 6 if bn <= 64 else 2
+    cw = 8
+    slots = (6 if wb <= 4 else 3) if bn <= 64 else 2
     v = ((108 if bn <= 128 else 216) * 1024 - slots * wb * 128 * cw * 4 - (128 * (bn + 8) * 4 if bn <= 64 else 0)
          - 4096) // (bn * 128)
     return max(2, min(8, v))
 
 
 @pytest.mark.parametrize("bn,cn,split", [(128, 1, 1), (128, 2, 1), (128, 4, 1), (256, 1, 1), (256, 2, 1),
-                                         (16, 1, 1), (16, 1, 3), (16, 1, 8), (64, 1, 1), (64, 1, 5)])
+                                         (16, 1, 2), (16, 1, 3), (16, 1, 8), (64, 1, 1), (64, 1, 5)])
 @pytest.mark.parametrize("wb,ab", [(5, 3), (2, 8)])
 def test_config_invariance_tc(bn, cn, split, wb, ab):
     """S:336 for the tcgen05 kernel: token tile width, cluster multicast and cluster split-K do not

@@ -7,8 +7,8 @@ from oracle import apt_oracle as O
 from synth import signed_codes
 
 def stg(wb, bn):
-    cw = 8 if wb <= 4 else 4
-    slots = 6 if bn <= 64 else 2
+    cw = 8
+    slots = (6 if wb <= 4 else 3) if bn <= 64 else 2
     v = ((108 if bn <= 128 else 216) * 1024 - slots * wb * 128 * cw * 4 - (128 * (bn + 8) * 4 if bn <= 64 else 0) - 4096) // (bn * 128)
     return max(2, min(8, v))
 

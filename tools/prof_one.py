@@ -16,9 +16,9 @@ def main():
     reps = int(sys.argv[6]) if len(sys.argv) > 6 else 3
     bn = int(sys.argv[7]) if len(sys.argv) > 7 else 0
     dev = torch.device("cuda")
-    W = P.pack(torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev), wb)
+    W = P.pack(torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev), wb, tiled=True)
     a = torch.randint(-(1 << (ab - 1)), 1 << (ab - 1), (m, k), dtype=torch.int8, device=dev)
-    A = P.pack(a, ab)
+    A = P.pack(a, ab, digits=True)
     ws = torch.rand(n, device=dev)
     cfg = P.select_config(m, n, k, wb, ab)
     if bn and cfg["kernel"] == 2:

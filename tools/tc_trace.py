@@ -12,7 +12,7 @@ import paper_2508_19087_b200 as P  # noqa: E402
 
 m, n, k, wb, ab = (int(v) for v in (sys.argv[1:6] if len(sys.argv) > 5 else (2048, 4096, 4096, 4, 4)))
 dev = torch.device("cuda")
-W = P.pack(torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev), wb)
+W = P.pack(torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev), wb, tiled=True)
 A = P.pack(torch.randint(-(1 << (ab - 1)), 1 << (ab - 1), (m, k), dtype=torch.int8, device=dev), ab, digits=True)
 ws = torch.rand(n, device=dev)
 cfg = P.select_config(m, n, k, wb, ab)
