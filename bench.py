@@ -3,8 +3,8 @@
 
 Default workload (BASELINE.json configs[1], "llama2-7b-decode"): one STEP is the whole per-call
 hot path for every Llama-2-7B decode linear (N x K = 4096x4096, 11008x4096, 4096x11008) at
-M = 1, 8, 16 tokens and W1A2, W2A2, W3A4, W4A4 (36 cases): activation pack (apt_pack_bipolar) +
-bit-plane GEMM with the fused fp16 scale epilogue (apt_gemm).  Weight packing is offline (done
+M = 1, 8, 16 tokens and W1A2, W2A2, W3A4, W4A4 (36 cases): the 12 distinct activations packed
+(apt_pack_bipolar), then the 36 bit-plane GEMMs with the fused fp16 scale epilogue (apt_gemm).  Weight packing is offline (done
 once, timed separately and reported as `weight_pack`).  Two packed-weight sets (2 x 133 MB > L2)
 alternate between steps so weights stream from HBM.  Steps are replayed as CUDA graphs.
 
@@ -243,7 +243,9 @@ def main():
                 for (m, wb, ab, n, k) in CASES]
     cfgs = [P.select_config(m, shard[n], k, wb, ab) for (m, wb, ab, n, k) in CASES]
 
-    # ---- offline weight packing (a1), timed once
+    # ---- offline weight packing (a1), timed once (after one untimed pack per width loads the kernels)
+    for wb in wbits_set:
+        P.pack(codes(128, 256, wb), wb, tiled=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record()
@@ -255,57 +257,67 @@ def main():
     wpack_bytes = sum(c.numel() + P.kpad(c.shape[1]) * c.shape[0] * wb // 8 for (s, wb, n, k), c in W_codes.items())
     del W_codes
 
-    def step(wset, ev=None):
+    # one step = pack every distinct activation (m, abits, K) once (12 packs; the 4096x4096 and 11008x4096
+    # linears of a precision share their input), then the 36 GEMMs (+ the all-gather of each output at N>1)
+    def pack_step():
+        for key in A_codes:
+            P.pack(A_codes[key], key[1], out=A_buf[key])
+
+    def gemm_step(wset):
         for i, (m, wb, ab, n, k) in enumerate(CASES):
-            Ap = P.pack(A_codes[(m, ab, k)], ab, out=A_buf[(m, ab, k)])
-            if ev is not None:
-                ev[i][0].record()
-            P.gemm(W_packed[wset][(wb, n, k)], Ap, out_kind="f16", layout=layout, w_scale=W_scale[(wb, n, k)],
-                   a_scale=A_scale[m], out=outs[i], config=cfgs[i])
-            if ev is not None:
-                ev[i][1].record()
+            P.gemm(W_packed[wset][(wb, n, k)], A_buf[(m, ab, k)], out_kind="f16", layout=layout,
+                   w_scale=W_scale[(wb, n, k)], a_scale=A_scale[m], out=outs[i], config=cfgs[i])
             if world > 1:
                 dist.all_gather_into_tensor(gathered[i], outs[i])
 
     log("eager warm steps")
-    # ---- capture instrumented step graphs (external timing events around every GEMM launch)
-    n_graphs = 2 * max(1, min(8, args.steps // 2))
-    graphs, events = [], []
-    step(0)
-    step(1)
+    for j in range(2):
+        pack_step()
+        gemm_step(j)
     barrier()
     use_graphs = True
     try:
-        for j in range(n_graphs):
-            ev = [(torch.cuda.Event(enable_timing=True, external=True),
-                   torch.cuda.Event(enable_timing=True, external=True)) for _ in CASES]
+        g_pack = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_pack, stream=stream):
+            pack_step()
+        g_gemm = []
+        for j in range(2):
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr, stream=stream):
-                step(j % 2, ev)
-            graphs.append(gr)
-            events.append(ev)
-    except Exception as exc:  # NCCL capture unsupported -> eager replay (still every kernel ours)
+                gemm_step(j)
+            g_gemm.append(gr)
+    except Exception as exc:  # NCCL capture unsupported -> eager launches (still every kernel ours)
         use_graphs = False
-        graphs, events = [], []
         print(f"[bench] graph capture failed ({exc!r}); timing eager steps", file=sys.stderr)
-        for j in range(n_graphs):
-            events.append([(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in CASES])
 
-    def run(j):
+    # events bracket the two phases of every step on the launching stream (none inside the graphs)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+
+    def run(j, marks=None):
+        if marks:
+            marks[0].record(stream)
         if use_graphs:
-            graphs[j % n_graphs].replay()
+            g_pack.replay()
         else:
-            step(j % 2, events[j % n_graphs])
+            pack_step()
+        if marks:
+            marks[1].record(stream)
+        if use_graphs:
+            g_gemm[j % 2].replay()
+        else:
+            gemm_step(j % 2)
+        if marks:
+            marks[2].record(stream)
 
     log(f"graphs={use_graphs}; warmup")
     for j in range(args.warmup):
         run(j)
     barrier()
     t_start = time.time()
-    e0.record()
+    e0.record(stream)
     for j in range(args.steps):
-        run(j)
-    e1.record()
+        run(j, ev[j])
+    e1.record(stream)
     barrier()
     t_end = time.time()
     ms = e0.elapsed_time(e1)
@@ -317,27 +329,15 @@ def main():
     ops_step = sum(2 * m * n * k for (m, wb, ab, n, k) in CASES)
     value = ops_step * args.steps / (ms * 1e-3) / 1e12
 
-    # ---- per-launch GEMM durations from the captured events (last replay of every graph)
-    dur = [statistics.mean(ev[i][0].elapsed_time(ev[i][1]) for ev in events) for i in range(len(CASES))]
-    gemm_ms = sum(dur)
+    # ---- GEMM phase duration per step, from the events of the timed region
+    gemm_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    pack_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     bytes_all = sum(alg_bytes(m, shard[n], k, wb, ab) for (m, wb, ab, n, k) in CASES)
     hbm_peak, peak_src = load_peaks()
     achieved = bytes_all / (gemm_ms * 1e-3) / 1e9
     traffic = load_traffic()
-    per_prec = {}
-    for (wb, ab) in PRECISIONS:
-        idx = [i for i, c in enumerate(CASES) if c[1] == wb and c[2] == ab]
-        per_prec[f"W{wb}A{ab}"] = round(sum(2 * CASES[i][0] * shard[CASES[i][3]] * CASES[i][4] for i in idx)
-                                        / (sum(dur[i] for i in idx) * 1e-3) / 1e12, 3)
-    per_m = {}
-    for m in MS:
-        idx = [i for i, c in enumerate(CASES) if c[0] == m]
-        per_m[f"M{m}"] = {"gemm_us_avg": round(1e3 * sum(dur[i] for i in idx) / len(idx), 2),
-                          "eff_tops": round(sum(2 * m * shard[CASES[i][3]] * CASES[i][4] for i in idx)
-                                            / (sum(dur[i] for i in idx) * 1e-3) / 1e12, 3),
-                          "hbm_frac": round(sum(alg_bytes(m, shard[CASES[i][3]], CASES[i][4], CASES[i][1], CASES[i][2])
-                                                for i in idx) / (sum(dur[i] for i in idx) * 1e-3) / 1e9 / hbm_peak, 4)}
-
+    per_prec, per_m = breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, shard, layout,
+                                use_graphs, hbm_peak)
     line = {"metric": METRIC, "value": round(value, 4), "unit": "TOPS",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -348,14 +348,18 @@ def main():
                        "l2": "inputs larger than L2: 2 alternating packed-weight sets (2 x 133 MB)",
                        "parallelism": f"tp{world} (N-split + all-gather)" if world > 1 else "single GPU",
                        "cuda_graphs": use_graphs},
-            "gpu_launches": 2 * len(CASES) * args.steps,
-            "roofline": {"bound": "hbm", "kernel": "gemm_mma_kernel (decode bit-plane GEMM)",
+            "gpu_launches": (len(A_codes) + len(CASES)) * args.steps,
+            "roofline": {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 bit-plane GEMM, 36 launches/step)",
+                         "measured": "GEMM phase of every timed step (events around the graph of 36 GEMM launches"
+                                     + (" + all-gathers" if world > 1 else "") + ")",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4),
                          "traffic": traffic.get("dram_bytes_per_launch_avg") if traffic else None,
                          "alg_bytes_per_launch_avg": round(bytes_all / len(CASES)),
-                         "gemm_share_of_step": round(gemm_ms / ms_per_step, 3)},
-            "per_precision_gemm_tops": per_prec, "per_m": per_m,
+                         "gemm_share_of_step": round(gemm_ms / ms_per_step, 3),
+                         "gemm_us_per_launch": round(1e3 * gemm_ms / len(CASES), 3)},
+            "act_pack": {"launches_per_step": len(A_codes), "us_per_step": round(1e3 * pack_ms, 3)},
+            "per_precision": per_prec, "per_m": per_m,
             "weight_pack": {"ms": round(wpack_ms, 3), "GB/s": round(wpack_bytes / (wpack_ms * 1e-3) / 1e9, 1)}}
 
     log("baselines")
@@ -370,6 +374,50 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, shard, layout, use_graphs, hbm_peak):
+    """GEMM-only throughput per precision and per M (outside the timed region): a graph of that group's
+    GEMMs (packed activations resident), replayed 10x per weight set with a 256 MB write between
+    replays so every replay streams its weights from HBM; events around each replay."""
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=stream.device)
+
+    def group_stats(idx):
+        gs = []
+        for wset in range(2):
+            def fn():
+                for i in idx:
+                    m, wb, ab, n, k = CASES[i]
+                    P.gemm(W_packed[wset][(wb, n, k)], A_buf[(m, ab, k)], out_kind="f16", layout=layout,
+                           w_scale=W_scale[(wb, n, k)], a_scale=A_scale[m], out=outs[i], config=cfgs[i])
+            fn()
+            if use_graphs:
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    fn()
+                gs.append(gr.replay)
+            else:
+                gs.append(fn)
+        ts = []
+        for r in range(20):
+            flush.fill_(r & 255)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            gs[r % 2]()
+            b.record(stream)
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        ms = statistics.median(x.elapsed_time(y) for x, y in ts)
+        ops = sum(2 * CASES[i][0] * shard[CASES[i][3]] * CASES[i][4] for i in idx)
+        byt = sum(alg_bytes(CASES[i][0], shard[CASES[i][3]], CASES[i][4], CASES[i][1], CASES[i][2]) for i in idx)
+        return {"gemm_us_avg": round(1e3 * ms / len(idx), 2), "eff_tops": round(ops / (ms * 1e-3) / 1e12, 3),
+                "hbm_frac": round(byt / (ms * 1e-3) / 1e9 / hbm_peak, 4)}
+
+    per_prec = {f"W{wb}A{ab}": group_stats([i for i, c in enumerate(CASES) if c[1] == wb and c[2] == ab])
+                for (wb, ab) in PRECISIONS}
+    per_m = {f"M{m}": group_stats([i for i, c in enumerate(CASES) if c[0] == m]) for m in MS}
+    del flush
+    return per_prec, per_m
 
 
 def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout, value, barrier):
@@ -394,9 +442,9 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
     def e2e_step(wset):
         for key in h_a:
             d_a[key].copy_(h_a[key], non_blocking=True)
+            P.pack(d_a[key], key[1], out=bufs[key])
         for i, (m, wb, ab, n, k) in enumerate(CASES):
-            Ap = P.pack(d_a[(m, ab, k)], ab, out=bufs[(m, ab, k)])
-            P.gemm(W_packed[wset][(wb, n, k)], Ap, out_kind="f16", layout=layout, w_scale=W_scale[(wb, n, k)],
+            P.gemm(W_packed[wset][(wb, n, k)], bufs[(m, ab, k)], out_kind="f16", layout=layout, w_scale=W_scale[(wb, n, k)],
                    a_scale=A_scale[m], out=d_out[i], config=cfgs[i])
             h_out[i].copy_(d_out[i], non_blocking=True)
 
