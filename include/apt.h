@@ -63,10 +63,12 @@ typedef enum {
 
 typedef enum {
   APT_PACK_ROWS = 0,  /* planes[i][r][w]: plane-major, row-major words (the canonical layout)            */
-  APT_PACK_TILED = 1  /* planes[i][r/128][w/8][r%128][w%8]: every 128-row x 256-element slab of a plane is
-                         4 KB contiguous, so the GEMM streams weight tiles with one bulk copy per plane
-                         (rows padded to a multiple of 128; pad-row words are unspecified and never
-                         reach a result).  Accepted for weights by the tcgen05 kernel.                     */
+  APT_PACK_TILED = 1  /* planes[i][r/128][w/8][(w%8)/4][r%128][w%4]: every 128-row x 256-element slab of a
+                         plane is 4 KB contiguous (so the GEMM streams weight tiles with few large bulk
+                         copies), split into two 2 KB halves of 128 rows x 4 words (one 128-element K
+                         step each, read bank-conflict-free on chip).  Rows padded to a multiple of 128;
+                         pad-row words are unspecified and never reach a result.  Accepted for weights
+                         by the tcgen05 kernel.                                                           */
 } apt_pack_layout;
 
 /* The packed "unified matrix" (SPEC PackedPlanes S:35-41, with 32-bit words per P:252).

@@ -54,8 +54,7 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
     if (c->split_k > 1 && (c->bn > 64 || c->cluster_n != 1)) return APT_ERR_UNSUPPORTED;
     if (c->cluster_n > 1 && c->bn < 128) return APT_ERR_UNSUPPORTED;
     if (c->bn == 16) {  // the up-front token slab holds at most 16 K steps per CTA
-      const int nch = (kw / 4 + 1) / 2;
-      if ((nch + c->split_k - 1) / c->split_k * 2 > 16) return APT_ERR_UNSUPPORTED;
+      if ((kw / 4 + c->split_k - 1) / c->split_k > 16) return APT_ERR_UNSUPPORTED;
     }
     return APT_OK;
   }
@@ -141,14 +140,14 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
     out->bn = M <= 16 ? 16 : 64;
     out->cluster_n = 1;
     const int64_t tiles = (int64_t)ceil_div(N, 128) * ceil_div(M, out->bn);
-    const int chunks = (kw / 4 + 1) / 2;  // 256-element weight chunks
+    const int steps = kw / 4;  // 128-element K steps
     int split = (int)((2 * kNumSMs + tiles / 2) / tiles);
     if (split > 8) split = 8;
-    if (split > chunks) split = chunks;
+    if (split > steps) split = steps;
     if (split < 1) split = 1;
-    if (out->bn == 16) {  // at most 16 K steps (8 chunks) per CTA, else the ring-buffered 64-token tile
-      while (split < 8 && (chunks + split - 1) / split > 8) ++split;
-      if ((chunks + split - 1) / split > 8) out->bn = 64;
+    if (out->bn == 16) {  // at most 16 K steps per CTA, else the ring-buffered 64-token tile
+      while (split < 8 && (steps + split - 1) / split > 16) ++split;
+      if ((steps + split - 1) / split > 16) out->bn = 64;
     }
     out->split_k = split;
   }

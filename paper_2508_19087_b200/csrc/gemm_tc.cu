@@ -41,6 +41,25 @@ __device__ long long g_tc_trace[8][512];
 #else
 #define TRACE(slot, ks) do { } while (0)
 #endif
+#ifdef APT_TC_GTRACE
+// grid-wide globaltimer timeline: [cta][phase], phases 0 entry 1 setup 2 first W 3 tokens 4 acc_full
+// 5 split-K push start 6 exit 7 smid 8 prefetch issued 9 partials received (profiling builds only)
+__device__ unsigned long long g_tc_gtrace[8192][16];
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// recorded in shared memory (a global store before a release fence would be waited for) and
+// copied out once at the end
+#define GTRACE(ph) do { s_gt[ph] = (ph) == 7 ? (unsigned long long)smid_u32() : gtimer_ns(); } while (0)
+#define GTRACE_DUMP() do { const int c_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+  if (c_ < 8192) for (int i_ = 0; i_ < 16; ++i_) g_tc_gtrace[c_][i_] = s_gt[i_]; } while (0)
+__device__ __forceinline__ uint32_t smid_u32() { uint32_t r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
+#else
+#define GTRACE(ph) do { } while (0)
+#define GTRACE_DUMP() do { } while (0)
+#endif
 
 // ------------------------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -139,10 +158,10 @@ struct TcSmem {
   static constexpr int kWBytes = WB * kTcBM * kCW * 4;  // weight planes per chunk
   static constexpr int kBOff = 0;
   static constexpr int kWOff = (kBAll ? kBAllSteps : STAGES) * kBBytes;
-  static constexpr int kRbOff = kWOff + kWSlots * kWBytes;       // split-K receive buffer [128][BN] i32
+  static constexpr int kRbOff = kWOff + kWSlots * kWBytes;       // split-K receive buffer: [S][128][cpr], cpr = ceil(BN / S), so S * cpr <= BN + S - 1 <= BN + 7
   static constexpr int kEpOff = kRbOff + (BN <= 64 ? kTcBM * (BN + 8) * 4 : 0);  // rw[128] ws[128] ra[BN] as[BN]
   static constexpr int kBarOff = kEpOff + (2 * kTcBM + 2 * BN) * 4;
-  static constexpr int kNumBars = 2 * STAGES + 2 * kWSlots + 2 * kTcAStages + 1;
+  static constexpr int kNumBars = 2 * STAGES + 2 * kWSlots + 2 * kTcAStages + 4;
   static constexpr int kTotal = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
 };
 
@@ -194,6 +213,9 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
                                                          const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
   using L = TcSmem<WB, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
+#ifdef APT_TC_GTRACE
+  __shared__ unsigned long long s_gt[16];  // phases a launch does not reach hold garbage
+#endif
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
@@ -224,13 +246,69 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
   const int S = gridDim.z;             // K split (cluster along z)
   const uint32_t crank = (CN > 1 || S > 1) ? cluster_ctarank() : 0u;
   // this CTA's K steps, in whole weight chunks
+  // this CTA's K steps [kb, ke): an even split at step granularity (a weight chunk is two steps
+  // relative to kb; the tile-major layout keeps steps contiguous across chunk boundaries)
   const int nk = p.k_words / 4;
-  const int nch = (nk + L::kKpc - 1) / L::kKpc;
-  const int kb = min(nk, (int)((blockIdx.z * nch) / S) * L::kKpc);
-  const int ke = min(nk, (int)(((blockIdx.z + 1) * nch) / S) * L::kKpc);
+  const int kb = (int)(((int64_t)blockIdx.z * nk) / S);
+  const int ke = (int)(((int64_t)(blockIdx.z + 1) * nk) / S);
   const int nloc = ke - kb;
   pdl_launch_dependents();
-  if (threadIdx.x == 0) TRACE(6, 0);
+  if (threadIdx.x == 0) { TRACE(6, 0); GTRACE(0); GTRACE(7); }
+
+  // split-K over DSMEM (BN <= 64, CN == 1): rank q reduces token columns [q*cpr, q*cpr + ncols(q))
+  const bool dsm = BN <= 64 && S > 1;
+  const int cpr = (BN + S - 1) / S;
+  auto ncols = [&](int q) { return max(0, min(cpr, BN - q * cpr)); };
+  const uint32_t red_full = acc_full + 8u;
+  const uint32_t wbig0 = acc_full + 16u;  // up-front weight prefetch, first chunk (one phase only)
+  const uint32_t wbig = acc_full + 24u;   // up-front weight prefetch, the rest (one phase only)
+
+  // tile-major weights (APT_PACK_TILED): a plane's K steps are contiguous 2 KB blocks in HBM, so the
+  // ring is plane-major [plane][slot][2 steps x 2 KB] and a run of steps moves with one bulk copy per
+  // plane (fewer, larger requests).  Canonical planes: one 3-D TMA box per chunk, chunk-major ring.
+  const bool tiled = p.w_tiled != 0;
+  const uint32_t* wtile = p.wp + (int64_t)(n0 >> 7) * (p.k_words >> 3) * 1024;
+  auto w_run = [&](int j0, int steps, int slot, uint32_t bar) {  // steps [j0, j0 + steps) -> slot..
+#pragma unroll
+    for (int i = 0; i < WB; ++i)
+      bulk_load(sW + (i * L::kWSlots + slot) * 4096, wtile + (int64_t)i * p.w_pstride + (int64_t)(kb + j0) * 512,
+                (uint32_t)steps * 2048, bar);
+  };
+  auto issue_w = [&](int c) {  // weight chunk c (local steps 2c, 2c + 1)
+    const int slot = c % L::kWSlots;
+    mbar_wait(wempty(slot), ((c / L::kWSlots) & 1) ^ 1);
+    if (tiled) {
+      const int steps = min(2, nloc - 2 * c);
+      mbar_expect_tx(wfull(slot), (uint32_t)(steps * 2048 * WB));
+      w_run(2 * c, steps, slot, wfull(slot));
+    } else {
+      mbar_expect_tx(wfull(slot), L::kWBytes);
+      tma_load_3d(sW + slot * L::kWBytes, &tm_w, wfull(slot), (kb + 2 * c) * 4, n0, 0);
+    }
+  };
+  const int n_pre = min(L::kWSlots, (nloc + 1) / 2);
+  const int pre_s0 = min(2, min(nloc, 2 * n_pre));  // steps in the first prefetch run
+  auto issue_pre = [&]() {
+    if (tiled) {
+      // the first ring's worth of steps in two runs per plane: chunk 0 (conversion starts as soon as
+      // it lands) and the rest
+      const int pre = min(nloc, 2 * n_pre);
+      const int s0 = pre_s0;
+      if (s0 > 0) {
+        mbar_expect_tx(wbig0, (uint32_t)(s0 * 2048 * WB));
+        w_run(0, s0, 0, wbig0);
+      }
+      if (pre > s0) {
+        mbar_expect_tx(wbig, (uint32_t)((pre - s0) * 2048 * WB));
+        w_run(s0, pre - s0, s0 / 2, wbig);
+      }
+      // phase 0 of the slots' own barriers is not used by these chunks: complete it now, so that a
+      // slot's second use (chunk c + kWSlots) is its phase 1
+      for (int c = 0; c < n_pre; ++c) mbar_arrive(wfull(c));
+    } else {
+      for (int c = 0; c < n_pre; ++c) issue_w(c);
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -246,56 +324,63 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
       mbar_init(a_empty(a), 1);
     }
     mbar_init(acc_full, 1);
+    mbar_init(red_full, 1);
+    mbar_init(wbig0, 1);
+    mbar_init(wbig, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0 && lane == 0) {
+    // the partial tiles this rank will receive (st.async complete_tx from every rank, itself included)
+    if (dsm) mbar_expect_tx(red_full, (uint32_t)(S * kTcBM * ncols((int)crank) * 4));
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_w) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_b) : "memory");
+    // weights never depend on the previous kernel (programmatic dependent launch) and need nothing
+    // but this thread's barriers: the first ring's worth of chunks is requested before the rest of
+    // the setup (TMEM allocation, CTA / cluster barriers)
+#ifndef APT_TC_LATE_W
+    if (CN == 1) issue_pre();
+#endif
+    GTRACE(8);
   }
+  if (warp == 4 && lane == 0) GTRACE(12);
   if (warp == 2) {
+    if (lane == 0) GTRACE(10);
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (lane == 0) GTRACE(11);
   }
   tc_fence_before();
-  if (CN > 1 || S > 1) cluster_sync_all(); else __syncthreads();
+  if (CN > 1) {
+    cluster_sync_all();  // multicast writes into peers from the first token tile on
+  } else {
+    __syncthreads();
+    // split-K peers are first touched at the reduction: arrive now, wait right before it.  Relaxed:
+    // the barrier inits are already released by fence.mbarrier_init, and a release arrive would wait
+    // for this thread's outstanding weight bulk copies (~1-2 us)
+    if (dsm) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  }
   tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
-  if (threadIdx.x == 0) TRACE(6, 1);
+  if (threadIdx.x == 0) { TRACE(6, 1); GTRACE(1); }
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      auto issue_w = [&](int c) {  // weight chunk c: all planes of 128 rows x kCW words
-        const int ks = kb + c * L::kKpc;
-        mbar_wait(wempty(c % L::kWSlots), ((c / L::kWSlots) & 1) ^ 1);
-        mbar_expect_tx(wfull(c % L::kWSlots), L::kWBytes);
-        const uint32_t dstW = sW + (c % L::kWSlots) * L::kWBytes;
-        if (p.w_tiled) {
-          // tile-major planes: each plane's 128-row x 8-word slab is 4 KB contiguous
-          const uint32_t* src = p.wp + ((int64_t)(n0 >> 7) * (p.k_words >> 3) + (ks >> 1)) * 1024;
-#pragma unroll
-          for (int i = 0; i < WB; ++i)
-            bulk_load(dstW + i * 4096, src + (int64_t)i * p.w_pstride, 4096, wfull(c % L::kWSlots));
-        } else {
-          tma_load_3d(dstW, &tm_w, wfull(c % L::kWSlots), ks * 4, n0, 0);
-        }
-      };
-      // weights never depend on the previous kernel: the first ring's worth of chunks is requested
-      // before waiting for it (programmatic dependent launch)
-      const int n_pre = min(L::kWSlots, (nloc + L::kKpc - 1) / L::kKpc);
-      for (int c = 0; c < n_pre; ++c) issue_w(c);
+#ifndef APT_TC_LATE_W
+      if (CN > 1)
+#endif
+        issue_pre();
       pdl_wait();
       if constexpr (L::kBAll) {
-        // the whole token slab of this CTA's K range, one barrier
+        // the whole token slab of this CTA's K range, one barrier.  (Requesting it from another warp
+        // ahead of the weight prefetch measured 5% slower in back-to-back launches.)
         mbar_expect_tx(full(0), (uint32_t)(nloc * L::kBBytes));
         for (int j = 0; j < nloc; ++j) tma_load_2d(sB + j * L::kBBytes, &tm_b, full(0), (kb + j) * kTcBK, m0);
       }
       for (int j = 0; j < nloc; ++j) {
         const int ks = kb + j;
-        if (j % L::kKpc == 0 && j / L::kKpc >= n_pre) {  // next weight chunk
-          issue_w(j / L::kKpc);
+        if (j % 2 == 0 && j / 2 >= n_pre) {  // next weight chunk
+          issue_w(j / 2);
         }
         if constexpr (L::kBAll) continue;
         const int s = j % STAGES;
@@ -324,6 +409,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
         const uint32_t pa = (j / kTcAStages) & 1;
         if (!L::kBAll || j == 0) mbar_wait(full(L::kBAll ? 0 : s), L::kBAll ? 0u : ph);
         TRACE(1, j);
+        if (j == 0) GTRACE(3);
         mbar_wait(a_full(a), pa);
         TRACE(2, j);
         tc_fence_after();
@@ -361,15 +447,23 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
     const int cw = warp - 4, sub = cw & 3, par = cw >> 2;
     const int r = sub * 32 + lane;       // row within the tile (= TMEM lane)
     const uint32_t lane_off = (uint32_t)(sub * 32) << 16;
+#ifdef APT_CONV_PIPE
+    int pend_a = -1;  // A stage whose tcgen05.st is still in flight
+#endif
     for (int j = par; j < nloc; j += 2) {
       const int c = j / L::kKpc, q = j % L::kKpc;  // kKpc == 2: each parity reads one step per chunk
-      mbar_wait(wfull(c % L::kWSlots), (c / L::kWSlots) & 1);
-      if (lane == 0 && cw == 0) TRACE(3, j);
+      if (tiled && c < n_pre) mbar_wait(2 * c < pre_s0 ? wbig0 : wbig, 0);
+      else mbar_wait(wfull(c % L::kWSlots), (c / L::kWSlots) & 1);
+      if (lane == 0 && (cw & 3) == 0) TRACE(3, j);
+      if (lane == 0 && cw == 0 && j == 0) GTRACE(2);
       uint4 v[WB];
-      const uint8_t* wsm = gbase + L::kWOff + (c % L::kWSlots) * L::kWBytes;
+      const uint8_t* wsm = gbase + L::kWOff;
 #pragma unroll
-      for (int i = 0; i < WB; ++i)
-        v[i] = *reinterpret_cast<const uint4*>(wsm + ((i * kTcBM + r) * L::kCW + 4 * q) * 4);
+      for (int i = 0; i < WB; ++i) {
+        const int off = tiled ? (i * L::kWSlots + c % L::kWSlots) * 4096 : (c % L::kWSlots) * L::kWBytes + i * 4096;
+        // tile-major: [q][row][4 words] (lanes read consecutive 16 B); canonical TMA box: [row][8 words]
+        v[i] = *reinterpret_cast<const uint4*>(wsm + off + (p.w_tiled ? q * 2048 + r * 16 : (r * L::kCW + 4 * q) * 4));
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(wempty(c % L::kWSlots));
       uint32_t d[32];
@@ -384,6 +478,20 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
       }
       const int a = j % kTcAStages;
       const uint32_t pa = (j / kTcAStages) & 1;
+      if (lane == 0 && (cw & 3) == 0) TRACE(7, j);
+#ifdef APT_CONV_PIPE
+      // the previous step's TMEM store completed while this step was rebuilt: publish it now
+      if (pend_a >= 0) {
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full(pend_a));
+      }
+      mbar_wait(a_empty(a), pa ^ 1);
+      tc_fence_after();
+      tmem_st32<32>(tmem + lane_off + kAcol0 + 32 * a, d);
+      pend_a = a;
+#else
       mbar_wait(a_empty(a), pa ^ 1);
       tc_fence_after();
       tmem_st32<32>(tmem + lane_off + kAcol0 + 32 * a, d);
@@ -391,13 +499,22 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full(a));
-      if (lane == 0 && cw == 0) TRACE(4, j);
+#endif
+      if (lane == 0 && (cw & 3) == 0) TRACE(4, j);
     }
+#ifdef APT_CONV_PIPE
+    if (pend_a >= 0) {
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full(pend_a));
+    }
+#endif
     // ------------------------------------------------------------ epilogue
     // warp (sub, par) owns rows 32*sub.. and the token columns [par*BN/2, (par+1)*BN/2)
     asm volatile("bar.sync 1, 320;" ::: "memory");   // epilogue operands are in shared memory
     mbar_wait(acc_full, 0);
-    if (lane == 0 && cw == 0) TRACE(5, 0);
+    if (lane == 0 && cw == 0) { TRACE(5, 0); GTRACE(4); }
     tc_fence_after();
     constexpr int kHalf = BN / 2;
     constexpr int kChunk = kHalf < 32 ? kHalf : 32;
@@ -419,9 +536,13 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
       }
     } else if constexpr (BN <= 64) {
       // ---------------------------------------------------------- split-K: push partials over DSMEM
-      // the partial of token column col goes to cluster rank col % S, slot col / S
-      const int slots = (BN + S - 1) / S;
-      const uint32_t rb_local = smem_u32(rbuf);
+      // token column col goes to rank col / cpr, slot col % cpr of that rank's rbuf[src = crank][r][.],
+      // as st.async stores that count down the receiver's red_full barrier
+      __syncwarp();
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // peers' barriers initialised
+      if (lane == 0 && cw == 0) GTRACE(5);
+      const uint32_t rb_local = smem_u32(rbuf) + (uint32_t)(((int)crank * kTcBM + r) * cpr * 4);
+      const int vec = (cpr % 4 == 0) ? 4 : (cpr % 2 == 0) ? 2 : 1;
 #pragma unroll 1
       for (int c0 = par * kHalf; c0 < (par + 1) * kHalf; c0 += kChunk) {
         uint32_t acc[kChunk];
@@ -431,44 +552,59 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
           for (int jj = 0; jj < kChunk; ++jj) acc[jj] = 0u;
         }
 #pragma unroll
-        for (int jj = 0; jj < kChunk; ++jj) {
-          const int col = c0 + jj;
-          const uint32_t off = (uint32_t)((((int)crank * kTcBM + r) * slots + col / S) * 4);
-          uint32_t remote;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(rb_local + off), "r"(col % S));
-          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(remote), "r"(acc[jj]) : "memory");
+        for (int jj = 0; jj < kChunk; jj += 4) {
+#pragma unroll
+          for (int h = 0; h < 4; h += vec) {
+            const int col = c0 + jj + h;
+            const int q = col / cpr;
+            uint32_t raddr, rbar;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(rb_local + (uint32_t)((col - q * cpr) * 4)), "r"(q));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(red_full), "r"(q));
+            if (vec == 4)
+              asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                           ::"r"(raddr), "r"(acc[jj + h]), "r"(acc[jj + h + 1]), "r"(acc[jj + h + 2]), "r"(acc[jj + h + 3]),
+                           "r"(rbar) : "memory");
+            else if (vec == 2)
+              asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];"
+                           ::"r"(raddr), "r"(acc[jj + h]), "r"(acc[jj + h + 1]), "r"(rbar) : "memory");
+            else
+              asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                           ::"r"(raddr), "r"(acc[jj + h]), "r"(rbar) : "memory");
+          }
+        }
+      }
+      __syncwarp();
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // exit guard (see below)
+      // this rank's columns: the sum of the S partials, then the epilogue
+      mbar_wait_cluster(red_full, 0);
+      if (lane == 0 && cw == 0) GTRACE(9);
+      const int nc = ncols((int)crank);
+      for (int sl = par; sl < nc; sl += 2) {
+        const int col = (int)crank * cpr + sl;
+        const int m = m0 + col;
+        if (m < p.e.M && n < p.e.N) {
+          uint32_t U = 0;
+          for (int src = 0; src < S; ++src) U += (uint32_t)rbuf[(src * kTcBM + r) * cpr + sl];
+          epilogue_store_v(p.e, m, n, U, ep_ra[col], rw, wsc, ep_as[col]);
         }
       }
     }
   }
-  if (BN <= 64 && S > 1) {
-    // every rank sums the partials of its token columns (col = rank + S * slot) and stores them
-    const int slots = (BN + S - 1) / S;
-    if (warp == 4 && lane == 0) TRACE(5, 3);
-    __syncwarp();  // reconverge the role-divergent warps: the cluster barrier is .aligned
-    cluster_sync_all();
-    if (warp == 4 && lane == 0) TRACE(5, 4);
-    if (warp >= 4) {
-      const int cw = warp - 4, sub = cw & 3, par = cw >> 2;
-      const int r = sub * 32 + lane;
-      const int n = n0 + r;
-      for (int sl = par; sl < slots; sl += 2) {
-        const int col = (int)crank + S * sl;
-        const int m = m0 + col;
-        if (col < BN && m < p.e.M && n < p.e.N) {
-          uint32_t U = 0;
-          for (int src = 0; src < S; ++src) U += (uint32_t)rbuf[(src * kTcBM + r) * slots + sl];
-          epilogue_store_v(p.e, m, n, U, ep_ra[col], ep_rw[r], ep_ws[r], ep_as[col]);
-        }
-      }
-    }
+  if (dsm && warp < 4) {
+    // the other warps take part in both cluster barrier phases
+    __syncwarp();
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   }
   if (warp == 4 && lane == 0) TRACE(5, 1);
   if (threadIdx.x == 0) TRACE(5, 2);
   tc_fence_before();
   __syncwarp();  // reconverge the role-divergent warps before the .aligned barriers
-  // no CTA may leave while cluster peers can still multicast into it or arrive on its barriers
-  if (CN > 1) cluster_sync_all(); else __syncthreads();
+  // no CTA may leave while cluster peers can still multicast / st.async into it or signal its barriers
+  if (CN > 1) cluster_sync_all();
+  else if (dsm) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else __syncthreads();
+  if (threadIdx.x == 0) { GTRACE(6); GTRACE_DUMP(); }
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
@@ -521,6 +657,8 @@ static cudaError_t launch_tc4(const CUtensorMap& tw, const CUtensorMap& tb, cons
                               cudaStream_t stream) {
   using L = TcSmem<WB, BN, ST>;
   static_assert(L::kTotal <= 227 * 1024, "shared memory budget");
+  // the decode tiles are sized for two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
+  static_assert(BN != 16 || 2 * (L::kTotal + 1024) <= 228 * 1024, "two CTAs per SM");
   auto kern = gemm_tc_kernel<WB, BN, ST, CN>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
   if (err != cudaSuccess) return err;
@@ -586,6 +724,11 @@ cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, in
 
 }  // namespace apt
 
+#ifdef APT_TC_GTRACE
+extern "C" __attribute__((visibility("default"))) int apt_debug_tc_gtrace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, apt::g_tc_gtrace, sizeof(unsigned long long) * (n < 8192 * 16 ? n : 8192 * 16));
+}
+#endif
 #ifdef APT_TC_TRACE
 extern "C" __attribute__((visibility("default"))) int apt_debug_tc_trace(long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, apt::g_tc_trace, sizeof(long long) * (n < 8 * 512 ? n : 8 * 512));

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(1024) pack_kernel(PackArgs p) {
       }
     }
     // planes: bit i of every element, element c -> bit c % 32 (LSB first)
-    uint32_t* dst = p.tiled ? p.planes + ((int64_t)(r >> 7) * (p.k_words >> 3) + (w >> 3)) * 1024 + (r & 127) * 8 + (w & 7)
+    uint32_t* dst = p.tiled ? p.planes + ((int64_t)(r >> 7) * (p.k_words >> 3) + (w >> 3)) * 1024 +
+                                  ((w >> 2) & 1) * 512 + (r & 127) * 4 + (w & 3)
                             : p.planes + (int64_t)r * p.k_words + w;
     uint32_t pw[BITS];
 #pragma unroll

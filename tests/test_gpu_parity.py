@@ -34,7 +34,8 @@ def _tiled_from_rows(planes):
     rb = -(-rows // 128)
     full = np.zeros((bits, rb * 128, kw), dtype=planes.dtype)
     full[:, :rows] = planes
-    return full.reshape(bits, rb, 128, kw // 8, 8).transpose(0, 1, 3, 2, 4)
+    # [bits][rb][kw/8][2][128][4]
+    return full.reshape(bits, rb, 128, kw // 8, 2, 4).transpose(0, 1, 3, 4, 2, 5)
 
 
 # ----------------------------------------------------------------------------- pack (T6)
@@ -59,10 +60,10 @@ def test_pack_tiled_layout(bits, rows, k):
     planes, rs = O.pack_planes(codes, bits)
     g = got.planes.cpu().numpy().view(np.uint32)
     rb = -(-rows // 128)
-    g = g.reshape(bits, rb, planes.shape[2] // 8, 128, 8)
+    g = g.reshape(bits, rb, planes.shape[2] // 8, 2, 128, 4)
     want = _tiled_from_rows(planes)
     for r in range(rows):
-        assert np.array_equal(g[:, r // 128, :, r % 128, :], want[:, r // 128, :, r % 128, :])
+        assert np.array_equal(g[:, r // 128, :, :, r % 128, :], want[:, r // 128, :, :, r % 128, :])
     assert np.array_equal(got.row_sum.cpu().numpy().astype(np.int64), rs)
 
 

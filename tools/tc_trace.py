@@ -29,6 +29,6 @@ t0 = t[6, 0]
 nk = (-(-k // 256) * 256) // 128
 print("rc", rc, "setup", t[6, 1] - t0, "acc_full", t[5, 0] - t0, "pushed", t[5, 3] - t0, "cluster_barrier", t[5, 4] - t0,
       "epi_end", t[5, 1] - t0, "prod_end", t[5, 2] - t0)
-print("ks  prod_issue  mma_full  mma_afull  conv_full  conv_done")
+print("ks  prod_issue  mma_full  mma_afull  conv_full  conv_done  conv_rebuilt")
 for ks in range(nk):
-    print(ks, *[int(t[s, ks] - t0) for s in range(5)])
+    print(ks, *[int(t[s, ks] - t0) for s in (0, 1, 2, 3, 4, 7)])
