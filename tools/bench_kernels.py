@@ -45,6 +45,14 @@ def time_graph(fn, reps, warm=3):
     return best * 1e3  # us
 
 
+def tc_stages(wb, bn):
+    """Mirror of gemm_tc.cu tc_stages_ct (the stage count apt_gemm validates)."""
+    slots = (6 if wb <= 4 else 3) if bn <= 64 else 2
+    v = ((108 if bn <= 128 else 216) * 1024 - slots * wb * 128 * 8 * 4 - (128 * (bn + 8) * 4 if bn <= 64 else 0)
+         - 4096) // (bn * 128)
+    return max(2, min(8, v))
+
+
 def case(m, n, k, wb, ab, cfg=None, baselines=True, tag=""):
     dev = torch.device("cuda")
     wbytes = n * kpad(k) * wb // 8
@@ -95,7 +103,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--suite", default="all")
     ap.add_argument("--out", default="gpurun_out/kernels.jsonl")
-    ap.add_argument("--bn", type=int, default=0, help="force TC bn (128/256)")
+    ap.add_argument("--bn", type=int, default=0, help="force TC bn (128/256) for M > 64")
+    ap.add_argument("--cn", type=int, default=0, help="force TC cluster_n for M > 64")
     args = ap.parse_args()
     rows = []
     cases = []
@@ -119,11 +128,13 @@ def main():
     with open(args.out, "a") as f:
         for tag, m, n, k, wb, ab in cases:
             cfg = None
-            if args.bn and m > 64:
+            if (args.bn or args.cn) and m > 64:
                 cfg = P.select_config(m, n, k, wb, ab)
-                cfg["bn"] = args.bn
-                stage = args.bn * 128 + wb * 128 * 16
-                cfg["stages"] = max(2, min(6, ((110 if args.bn <= 128 else 220) * 1024) // stage))
+                if args.bn:
+                    cfg["bn"] = args.bn
+                    cfg["stages"] = tc_stages(wb, args.bn)
+                if args.cn:
+                    cfg["cluster_n"] = args.cn
             r = case(m, n, k, wb, ab, cfg=cfg, baselines=(tag != "sweep" or (wb, ab) in ((4, 4), (8, 8))), tag=tag)
             print(json.dumps(r), flush=True)
             f.write(json.dumps(r) + "\n")
