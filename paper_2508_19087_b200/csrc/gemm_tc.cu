@@ -45,6 +45,7 @@ __device__ long long g_tc_trace[8][512];
 // grid-wide globaltimer timeline: [cta][phase], phases 0 entry 1 setup 2 first W 3 tokens 4 acc_full
 // 5 split-K push start 6 exit 7 smid 8 prefetch issued 9 partials received (profiling builds only)
 __device__ unsigned long long g_tc_gtrace[8192][16];
+__device__ unsigned int g_tc_gtrace_next;  // next free row (reset by apt_debug_tc_gtrace_reset)
 __device__ __forceinline__ unsigned long long gtimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -53,7 +54,11 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
 // recorded in shared memory (a global store before a release fence would be waited for) and
 // copied out once at the end
 #define GTRACE(ph) do { s_gt[ph] = (ph) == 7 ? (unsigned long long)smid_u32() : gtimer_ns(); } while (0)
-#define GTRACE_DUMP() do { const int c_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+// rows are taken in exit order from a global counter, so consecutive launches land in distinct rows;
+// column 13 holds the CTA's linear index, 14 the grid size
+#define GTRACE_DUMP() do { const unsigned c_ = atomicAdd(&g_tc_gtrace_next, 1u); \
+  s_gt[13] = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+  s_gt[14] = gridDim.x * gridDim.y * gridDim.z; \
   if (c_ < 8192) for (int i_ = 0; i_ < 16; ++i_) g_tc_gtrace[c_][i_] = s_gt[i_]; } while (0)
 __device__ __forceinline__ uint32_t smid_u32() { uint32_t r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
 #else
@@ -371,6 +376,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
 #endif
         issue_pre();
       pdl_wait();
+      GTRACE(15);
       if constexpr (L::kBAll) {
         // the whole token slab of this CTA's K range, one barrier.  (Requesting it from another warp
         // ahead of the weight prefetch measured 5% slower in back-to-back launches.)
@@ -725,6 +731,11 @@ cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, in
 }  // namespace apt
 
 #ifdef APT_TC_GTRACE
+extern "C" __attribute__((visibility("default"))) int apt_debug_tc_gtrace_reset() {
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(apt::g_tc_gtrace_next, &z, sizeof(z));
+  return (int)cudaMemset(apt::g_tc_gtrace, 0, 0) ;
+}
 extern "C" __attribute__((visibility("default"))) int apt_debug_tc_gtrace(unsigned long long* host, int n) {
   return (int)cudaMemcpyFromSymbol(host, apt::g_tc_gtrace, sizeof(unsigned long long) * (n < 8192 * 16 ? n : 8192 * 16));
 }
