@@ -118,6 +118,21 @@ APT_API size_t apt_packed_plane_bytes(int32_t rows, int32_t k, int32_t bits, int
 APT_API apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k, int64_t ld, int32_t bits,
                             apt_encoding enc, apt_packed* out, int32_t* range_error, void* stream);
 
+/* Fused activation quantize + pack (reading R-Q).  Linear quantization
+ * x = s * x_hat + z with z = 0 and one scale per row (per token), then the same
+ * decomposition as apt_pack_bipolar, in one kernel:
+ *   s[r]        = RN_f32( max_{c<k} |x[r][c]| / (2^(bits-1) - 1) )
+ *   x_hat[r][c] = clamp( rint( RN_f32(x[r][c] / s[r]) ), -2^(bits-1), 2^(bits-1) - 1 ), 0 if s[r] == 0
+ * IEEE fp32 arithmetic (division rounded to nearest even, rint half-to-even); the codes are the
+ * signed encoding (APT_ENC_SIGNED).  Pass `scale` as apt_scales.a_scale of the following apt_gemm.
+ *   x     : fp16 (IEEE binary16, as uint16 bits) [rows][ld] row-major, finite values.
+ *   out   : as apt_pack_bipolar (caller-allocated planes / row_sum / optional digits, layout set).
+ *   scale : device fp32 [rows], written.
+ * Errors: APT_ERR_INVALID_ARGUMENT (null pointers, rows <= 0, k <= 0, ld < k, bits outside [2,8] —
+ *         a 1-bit symmetric grid has no positive level —, misaligned planes/digits), APT_ERR_CUDA. */
+APT_API apt_status apt_quantize_pack(const uint16_t* x, int32_t rows, int32_t k, int64_t ld, int32_t bits,
+                                     apt_packed* out, float* scale, void* stream);
+
 /* Per-channel / per-token fp32 scales for APT_OUT_F16_SCALED (reading Q10):
  *   out[m][n] = RN_fp16( ((float)Y[m][n] * w_scale[n]) * a_scale[m] ), fp32 arithmetic,
  *   one final round-to-nearest-even to fp16 (overflow -> +-inf). */

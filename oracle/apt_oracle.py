@@ -246,3 +246,35 @@ def scale_fp64(y: np.ndarray, w_scale: np.ndarray, a_scale: np.ndarray | None) -
 def scale_exact(y: int, ws: float, a_s: float) -> Fraction:
     """Exact rational value of Y*ws*as (pins ``scale_fp64``)."""
     return Fraction(int(y)) * Fraction(float(ws)) * Fraction(float(a_s))
+
+
+# --------------------------------------------------------------------------
+# §3.1 linear quantization (P:199-201), per-token symmetric: the step before
+# the pack (SURVEY §8f NEXT-1, DESIGN.md reading R-Q)
+# --------------------------------------------------------------------------
+
+def quantize_symmetric(x: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """P:199-201 "W = s W_hat + z" with z = 0 and one scale s per row (token),
+    for n-bit signed codes (n >= 2).  The integer decision is taken in IEEE
+    fp32, the precision of the CUDA kernel (tier rule: both sides decide in the
+    same precision):
+        s[r]      = fl32( max_c |x[r,c]| / (2^(n-1) - 1) )
+        x_hat[r,c] = clamp(rint(fl32(x[r,c] / s[r])), -2^(n-1), 2^(n-1)-1)   (0 if s = 0)
+    ``x`` holds fp16 values (any float array; converted to fp32 exactly).
+    Returns (int8 codes [rows, k], float32 scales [rows])."""
+    if n < 2 or n > 8:
+        raise ValueError("symmetric quantization needs n in [2, 8]")
+    x32 = np.asarray(x, dtype=np.float16).astype(np.float32)
+    qmax = np.float32((1 << (n - 1)) - 1)
+    codes = np.zeros(x32.shape, dtype=np.int8)
+    scales = np.zeros(x32.shape[0], dtype=np.float32)
+    lo, hi = signed_range(n)
+    for r in range(x32.shape[0]):
+        amax = np.float32(np.max(np.abs(x32[r]))) if x32.shape[1] else np.float32(0)
+        s = np.float32(amax / qmax)          # fp32 / fp32 -> IEEE round to nearest
+        scales[r] = s
+        if s == 0:
+            continue
+        q = np.rint(x32[r] / s)              # fp32 division, then half-to-even
+        codes[r] = np.clip(q, lo, hi).astype(np.int8)
+    return codes, scales

@@ -17,7 +17,7 @@ APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
 APT_KERNEL_AUTO, APT_KERNEL_MMA_SPLITK, APT_KERNEL_TC = 0, 1, 2
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
-EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_select_config", "apt_gemm_workspace_bytes",
+EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes",
             "apt_gemm", "apt_status_string", "apt_abi_version"]
 
 
@@ -61,6 +61,9 @@ def lib():
         L.apt_pack_bipolar.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                        ctypes.c_int32, ctypes.c_int, ctypes.POINTER(AptPacked), ctypes.c_void_p,
                                        ctypes.c_void_p]
+        L.apt_quantize_pack.restype = ctypes.c_int
+        L.apt_quantize_pack.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                        ctypes.c_int32, ctypes.POINTER(AptPacked), ctypes.c_void_p, ctypes.c_void_p]
         L.apt_select_config.restype = ctypes.c_int
         L.apt_select_config.argtypes = [ctypes.c_int32] * 5 + [ctypes.POINTER(AptConfig)]
         L.apt_gemm_workspace_bytes.restype = ctypes.c_size_t

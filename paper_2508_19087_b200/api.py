@@ -95,6 +95,26 @@ def pack(codes: torch.Tensor, bits: int, encoding: str = "signed", out: Packed |
     return out
 
 
+def quantize_pack(x: torch.Tensor, bits: int, out: Packed | None = None, scale: torch.Tensor | None = None,
+                  stream=None, digits: bool = True, tiled: bool = False) -> tuple[Packed, torch.Tensor]:
+    """apt_quantize_pack: fp16 activations [rows, k] -> (Packed signed codes, fp32 per-row scale).
+    Symmetric per-token quantization (z = 0) fused with the bit-plane pack; pass the scale
+    as ``a_scale`` of :func:`gemm`."""
+    _require_cuda(x, "x")
+    if x.dtype != torch.float16 or x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("x must be a 2-D float16 tensor with unit stride along K")
+    rows, k = x.shape
+    if out is None:
+        out = alloc_packed(rows, k, bits, x.device, digits=digits, tiled=tiled)
+    if scale is None:
+        scale = torch.empty(rows, dtype=torch.float32, device=x.device)
+    st = out.struct()
+    rc = L.lib().apt_quantize_pack(x.data_ptr(), rows, k, x.stride(0), bits, ctypes.byref(st), scale.data_ptr(),
+                                   _stream_handle(stream))
+    L.check("apt_quantize_pack", rc)
+    return out, scale
+
+
 def select_config(M: int, N: int, K: int, wbits: int, abits: int) -> dict:
     """apt_select_config (p = wbits, q = abits)."""
     c = L.AptConfig()

@@ -115,6 +115,34 @@ apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k, int64_
   return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
 }
 
+apt_status apt_quantize_pack(const uint16_t* x, int32_t rows, int32_t k, int64_t ld, int32_t bits,
+                             apt_packed* out, float* scale, void* stream) {
+  if (!x || !out || !out->planes || !out->row_sum || !scale) return APT_ERR_INVALID_ARGUMENT;
+  if (rows <= 0 || k <= 0 || ld < k || bits < 2 || bits > 8) return APT_ERR_INVALID_ARGUMENT;
+  if (!aligned16(out->planes)) return APT_ERR_INVALID_ARGUMENT;
+  if (out->digits && !aligned16(out->digits)) return APT_ERR_INVALID_ARGUMENT;
+  if (out->layout != APT_PACK_ROWS && out->layout != APT_PACK_TILED) return APT_ERR_INVALID_ARGUMENT;
+  out->rows = rows;
+  out->k = k;
+  out->k_words = (int32_t)(kpad_of(k) / 32);
+  out->bits = bits;
+  apt::PackArgs p;
+  p.codes = nullptr;
+  p.ld = ld;
+  p.rows = rows;
+  p.k = k;
+  p.k_words = out->k_words;
+  p.enc = APT_ENC_SIGNED;
+  p.planes = out->planes;
+  p.tiled = out->layout == APT_PACK_TILED ? 1 : 0;
+  p.plane_stride = (int64_t)(p.tiled ? (rows + 127) / 128 * 128 : rows) * out->k_words;
+  p.row_sum = out->row_sum;
+  p.range_error = nullptr;
+  p.digits = out->digits;
+  cudaError_t err = apt::launch_quant_pack(p, x, scale, bits, reinterpret_cast<cudaStream_t>(stream));
+  return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+}
+
 apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, apt_config* out) {
   if (!out || M <= 0 || N <= 0 || K <= 0 || wbits < 1 || wbits > 8 || abits < 1 || abits > 8)
     return APT_ERR_INVALID_ARGUMENT;

@@ -19,6 +19,8 @@ struct PackArgs {
   int32_t tiled;         // planes tile-major (APT_PACK_TILED)
 };
 cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream);
+// fused fp16 -> per-row symmetric quantize -> pack (x: const __half*, scale: [rows] fp32 out)
+cudaError_t launch_quant_pack(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream);
 
 struct MmaArgs {
   const uint32_t* wp;      // weight planes [wbits][N][k_words]

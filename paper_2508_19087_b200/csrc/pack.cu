@@ -10,6 +10,7 @@
 // and the eight nibbles of a plane form the output word (element c -> bit c%32, LSB first).
 // Row sums of the signed codes use dp4a; the CTA reduces them without atomics.
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -41,6 +42,51 @@ __device__ __forceinline__ uint32_t from_offset4(uint32_t u) {
     const uint32_t x = u ^ (h * 0x01010101u);                   // n-bit two's complement pattern
     const uint32_t s = (x >> (BITS - 1)) & 0x01010101u;         // sign bit of every byte
     return x | (s * (0x100u - 2u * h));                          // sign-extend (no cross-byte carry)
+  }
+}
+
+// One 32-element word of row r: offset digits u[8] (4 per uint32) -> the BITS plane words (element
+// c -> bit c % 32, LSB first) and, when requested, the kernel-order u8 digit view.
+template <int BITS>
+__device__ __forceinline__ void store_word(const PackArgs& p, int r, int w, const uint32_t (&u)[8]) {
+  // planes: bit i of every element, element c -> bit c % 32 (LSB first)
+  uint32_t* dst = p.tiled ? p.planes + ((int64_t)(r >> 7) * (p.k_words >> 3) + (w >> 3)) * 1024 +
+                                ((w >> 2) & 1) * 512 + (r & 127) * 4 + (w & 3)
+                          : p.planes + (int64_t)r * p.k_words + w;
+  uint32_t pw[BITS];
+#pragma unroll
+  for (int i = 0; i < BITS; ++i) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t nib = (((u[j] >> i) & 0x01010101u) * 0x01020408u) >> 24;
+      word |= nib << (4 * j);
+    }
+    dst[(int64_t)i * p.plane_stride] = word;
+    pw[i] = word;
+  }
+  if (p.digits) {
+    // the optional digit view: the same word through the kernels' operand rebuild
+    uint32_t d[8];
+    rebuild8<BITS>(pw, d);
+    uint4* dd = reinterpret_cast<uint4*>(p.digits + ((int64_t)r * p.k_words + w) * 32);
+    dd[0] = make_uint4(d[0], d[1], d[2], d[3]);
+    dd[1] = make_uint4(d[4], d[5], d[6], d[7]);
+  }
+}
+
+// CTA reduction of a row's signed-code sum (pads contribute 0) into p.row_sum[r]
+__device__ __forceinline__ void row_sum_store(const PackArgs& p, int r, int sum) {
+  __shared__ int red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int v = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) p.row_sum[r] = v;
   }
 }
 
@@ -112,43 +158,9 @@ __global__ void __launch_bounds__(1024) pack_kernel(PackArgs p) {
         }
       }
     }
-    // planes: bit i of every element, element c -> bit c % 32 (LSB first)
-    uint32_t* dst = p.tiled ? p.planes + ((int64_t)(r >> 7) * (p.k_words >> 3) + (w >> 3)) * 1024 +
-                                  ((w >> 2) & 1) * 512 + (r & 127) * 4 + (w & 3)
-                            : p.planes + (int64_t)r * p.k_words + w;
-    uint32_t pw[BITS];
-#pragma unroll
-    for (int i = 0; i < BITS; ++i) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t nib = (((u[j] >> i) & 0x01010101u) * 0x01020408u) >> 24;
-        word |= nib << (4 * j);
-      }
-      dst[(int64_t)i * p.plane_stride] = word;
-      pw[i] = word;
-    }
-    if (p.digits) {
-      // the optional digit view: the same word through the kernels' operand rebuild
-      uint32_t d[8];
-      rebuild8<BITS>(pw, d);
-      uint4* dd = reinterpret_cast<uint4*>(p.digits + ((int64_t)r * p.k_words + w) * 32);
-      dd[0] = make_uint4(d[0], d[1], d[2], d[3]);
-      dd[1] = make_uint4(d[4], d[5], d[6], d[7]);
-    }
+    store_word<BITS>(p, r, w, u);
   }
-  // CTA reduction of the row sum (pads contribute 0)
-  __shared__ int red[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int v = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) p.row_sum[r] = v;
-  }
+  row_sum_store(p, r, sum);
 }
 
 cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream) {
@@ -168,6 +180,98 @@ cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream) {
     default: return launch_pdl(pack_kernel<8>, grid, block, 0, stream, dim3(1, 1, 1), p);
   }
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused activation quantize + pack (reading R-Q): fp16 rows -> per-row
+// symmetric scale -> signed codes -> planes / digit view / row sums, one read of the row from HBM
+// (the second pass hits L1/L2).  Linear quantization x = s * x_hat + z with z = 0:
+//   s      = RN_f32( max_k |x| / (2^(n-1) - 1) )
+//   x_hat  = clamp( rint( RN_f32(x / s) ), -2^(n-1), 2^(n-1) - 1 )   (0 where s == 0)
+// in IEEE fp32 (division rounded to nearest, rint half-to-even), so the integer decision is taken in
+// the same precision as the oracle's.
+template <int BITS>
+__global__ void __launch_bounds__(1024) quant_pack_kernel(PackArgs p, const __half* __restrict__ x, float* scale) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int r = blockIdx.x;
+  const __half* row = x + (int64_t)r * p.ld;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0);
+  auto load32 = [&](int c0, float (&f)[32]) {
+    if (vec_ok && c0 + 32 <= p.k) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + c0) + q);
+        const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 g = __half22float2(h[t]);
+          f[8 * q + 2 * t] = g.x;
+          f[8 * q + 2 * t + 1] = g.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) f[e] = (c0 + e < p.k) ? __half2float(row[c0 + e]) : 0.f;
+    }
+  };
+  // pass 1: the row's absolute maximum
+  float amax = 0.f;
+  for (int w = threadIdx.x; w < p.k_words; w += blockDim.x) {
+    float f[32];
+    load32(w * 32, f);
+#pragma unroll
+    for (int e = 0; e < 32; ++e) amax = fmaxf(amax, fabsf(f[e]));
+  }
+  __shared__ float s_red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  float m = 0.f;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, s_red[i]);
+  constexpr float kQmax = (float)((1 << (BITS - 1)) - 1);
+  const float s = __fdiv_rn(m, kQmax);
+  if (threadIdx.x == 0) scale[r] = s;
+  // pass 2: codes -> planes
+  int sum = 0;
+  for (int w = threadIdx.x; w < p.k_words; w += blockDim.x) {
+    float f[32];
+    load32(w * 32, f);
+    uint32_t u[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        float q = s > 0.f ? rintf(__fdiv_rn(f[4 * j + b], s)) : 0.f;
+        q = fminf(fmaxf(q, -(kQmax + 1.f)), kQmax);
+        word |= ((uint32_t)(int)q & 0xFFu) << (8 * b);
+      }
+      sum = __dp4a((int)word, 0x01010101, sum);
+      u[j] = to_offset4<BITS>(word);
+    }
+    store_word<BITS>(p, r, w, u);
+  }
+  row_sum_store(p, r, sum);
+}
+
+cudaError_t launch_quant_pack(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {
+  int threads = ((p.k_words + 31) / 32) * 32;
+  if (threads > 1024) threads = 1024;
+  if (threads < 32) threads = 32;
+  dim3 grid(p.rows), block(threads);
+  const __half* xh = reinterpret_cast<const __half*>(x);
+  switch (bits) {
+    case 2: return launch_pdl(quant_pack_kernel<2>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale);
+    case 3: return launch_pdl(quant_pack_kernel<3>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale);
+    case 4: return launch_pdl(quant_pack_kernel<4>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale);
+    case 5: return launch_pdl(quant_pack_kernel<5>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale);
+    case 6: return launch_pdl(quant_pack_kernel<6>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale);
+    case 7: return launch_pdl(quant_pack_kernel<7>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale);
+    case 8: return launch_pdl(quant_pack_kernel<8>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace apt

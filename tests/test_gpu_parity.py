@@ -280,3 +280,59 @@ def test_llama7b_prefill_sampled(n, k, pw, pa):
     assert np.array_equal(got[rows], c_gemm_i64(a[rows], w))
     wsum = w.astype(np.int64).sum(0)
     assert np.array_equal(got.sum(1), a.astype(np.int64) @ wsum)
+
+
+# ----------------------------------------------------------------------------- fused quantize + pack (NEXT-1)
+
+@pytest.mark.parametrize("bits", range(2, 9))
+@pytest.mark.parametrize("rows,k", [(1, 1), (3, 33), (16, 4096), (5, 11008), (2, 1000)])
+def test_quantize_pack_matches_oracle(bits, rows, k):
+    """apt_quantize_pack vs oracle.quantize_symmetric + oracle.pack_planes: scales, planes, row sums
+    bit-exact; the digit view holds the same offset digits."""
+    from synth import fp16_activations
+    x = fp16_activations(rows, k, seed=bits * 1000 + rows + k)
+    if rows > 2:
+        x[2] = 0  # an all-zero row: s = 0, codes 0
+    Pk, s = P.quantize_pack(_dev(x), bits)
+    codes, so = O.quantize_symmetric(x, bits)
+    planes, rs = O.pack_planes(codes, bits)
+    torch.cuda.synchronize()
+    assert np.array_equal(s.cpu().numpy(), so)
+    assert np.array_equal(Pk.planes.cpu().numpy().view(np.uint32), planes)
+    assert np.array_equal(Pk.row_sum.cpu().numpy().astype(np.int64), rs)
+    dig = Pk.digits.cpu().numpy().astype(np.int64)
+    u = np.zeros((rows, O.kpad(k)), dtype=np.int64) + (1 << (bits - 1))
+    u[:, :k] = O.offset_bits_matrix(codes, bits)
+    assert np.array_equal(np.sort(dig.reshape(rows, -1, 32), axis=2), np.sort(u.reshape(rows, -1, 32), axis=2))
+
+
+def test_quantize_pack_ties_and_strides():
+    """Exact half-integer quotients (rint half-to-even) and a row stride > k."""
+    x = np.zeros((4, 300), dtype=np.float16)
+    x[:, 0] = 7.0                           # n = 4: s = 1.0 exactly
+    x[:, 1:15] = np.arange(-3.5, 3.5, 0.5)  # ties at +-0.5, +-1.5, ... and exact integers
+    big = np.zeros((4, 320), dtype=np.float16)
+    big[:, :300] = x
+    t = _dev(big)[:, :300]
+    Pk, s = P.quantize_pack(t, 4)
+    codes, so = O.quantize_symmetric(x, 4)
+    planes, _ = O.pack_planes(codes, 4)
+    assert np.array_equal(s.cpu().numpy(), so) and so[0] == 1.0
+    assert np.array_equal(Pk.planes.cpu().numpy().view(np.uint32), planes)
+
+
+@pytest.mark.parametrize("m,pa,pw", [(1, 4, 2), (16, 4, 4), (300, 8, 2)])
+def test_quantize_pack_then_gemm_f16(m, pa, pw):
+    """fp16 activations -> apt_quantize_pack -> apt_gemm(fp16, a_scale = the quantize scale) vs the
+    fp64-scaled oracle on the oracle's own codes and scales."""
+    from synth import fp16_activations
+    n, k = 384, 4096
+    x = fp16_activations(m, k, seed=m + 10 * pa)
+    w = signed_codes(n, k, pw, seed=5)
+    ws = log_uniform_scales(n, -10, -6, seed=6)
+    A, s = P.quantize_pack(_dev(x), pa)
+    W = P.pack(_dev(w), pw, tiled=True)
+    got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=s).cpu().numpy().astype(np.float64)
+    codes, so = O.quantize_symmetric(x, pa)
+    ref = O.scale_fp64(O.gemm_signed(codes, w), ws, so)
+    assert (np.abs(got - ref) <= 1e-3 * np.abs(ref) + 2.0 ** -24).all()

@@ -293,3 +293,64 @@ def test_int32_bound():
     assert not O.int32_bound_ok(33025, 8, 8)       # Kpad = 33280 -> 2163832000 >= 2^31
     assert O.int32_bound_ok(28672, 8, 8)           # largest BASELINE K
     assert O.kpad(28672) == 28672 and O.kpad(1) == 256 and O.kpad(257) == 512
+
+
+# ---------------------------------------------------------------- quantize (reading R-Q)
+def test_quantize_worked_example():
+    # n = 2: qmax = 1, s = max|x| = 1.0; 0.5 is a tie -> rint half-to-even -> 0; 0.75 -> 1
+    codes, s = O.quantize_symmetric(np.array([[0.5, -1.0, 0.25, 0.75]], dtype=np.float16), 2)
+    assert s.tolist() == [1.0]
+    assert codes.tolist() == [[0, -1, 0, 1]]
+    # n = 4: qmax = 7, s = fl32(3.5 / 7) = 0.5 exactly; x / s exact: 3.5 -> 7, -1.25 -> -2.5 -> -2, 0.75 -> 1.5 -> 2
+    codes, s = O.quantize_symmetric(np.array([[3.5, -1.25, 0.75, 0.0]], dtype=np.float16), 4)
+    assert s.tolist() == [0.5]
+    assert codes.tolist() == [[7, -2, 2, 0]]
+
+
+def test_quantize_zero_row_and_range():
+    codes, s = O.quantize_symmetric(np.zeros((2, 5), dtype=np.float16), 3)
+    assert s.tolist() == [0.0, 0.0] and not codes.any()
+    with pytest.raises(ValueError):
+        O.quantize_symmetric(np.ones((1, 4), dtype=np.float16), 1)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8])
+def test_quantize_exact_rational_properties(n):
+    """Pins against exact arithmetic (fractions), not the formula: s is the fp32 nearest to
+    max|x| / qmax; every code is the integer nearest to the exact x / s (away from near-ties, where
+    the fp32 quotient may legitimately decide), the row maximum maps to +-qmax, and the dequantised
+    value is within s/2 of x (P:199-201 linear quantization with z = 0)."""
+    rng = np.random.default_rng(100 + n)
+    x = (rng.standard_normal((6, 97)) * rng.choice([1e-3, 1.0, 30.0], size=(6, 1))).astype(np.float16)
+    x[2, :] = np.float16(0)
+    x[2, 5] = np.float16(-2.0)
+    codes, s = O.quantize_symmetric(x, n)
+    qmax = (1 << (n - 1)) - 1
+    for r in range(x.shape[0]):
+        xr = [Fraction(float(v)) for v in x[r]]
+        amax = max(abs(v) for v in xr)
+        exact = amax / qmax
+        sr = Fraction(float(s[r]))
+        # fp32 round-to-nearest: relative error <= 2^-24
+        assert abs(sr - exact) <= exact * Fraction(1, 1 << 24)
+        if amax == 0:
+            assert not codes[r].any()
+            continue
+        imax = max(range(len(xr)), key=lambda c: abs(xr[c]))
+        assert abs(int(codes[r, imax])) == qmax
+        for c, v in enumerate(xr):
+            t = v / sr
+            q = int(codes[r, c])
+            assert -(qmax + 1) <= q <= qmax
+            assert abs(v - sr * q) <= sr / 2 * (1 + Fraction(1, 1 << 20))
+            frac = t - (t.numerator // t.denominator)
+            if abs(frac - Fraction(1, 2)) > Fraction(1, 1 << 18):
+                assert q == round(t)
+
+
+def test_quantize_power_of_two_invariance():
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((3, 64)).astype(np.float16)
+    c1, s1 = O.quantize_symmetric(x, 4)
+    c2, s2 = O.quantize_symmetric((x.astype(np.float32) * 8).astype(np.float16), 4)
+    assert np.array_equal(c1, c2) and np.array_equal(s2, s1 * 8)
