@@ -157,11 +157,13 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
   out->bk = 128;
   out->cta_pair = 0;
   if (M > 64) {
-    // prefill: 128 weight rows x 128 tokens per CTA, two CTAs per SM, the token tile multicast to a
-    // cluster of up to 4 weight tiles
-    out->bn = wbits > 4 ? 256 : 128;  // wide weight chunks leave room for one 256-token CTA per SM
+    // prefill: 128 weight rows x 256 tokens per CTA, one CTA per SM, no cluster.  The weight rebuild
+    // (converter warps, integer ALU) is paid once per 256 tokens instead of 128; measured on B200
+    // (profiles/r1_prefill_bn_sweep.txt) 1.0-1.4x faster than 2 x (128 x 128) CTAs per SM with the
+    // token tile multicast to a 4-CTA cluster, and faster than the 256-token tile in 2-CTA clusters
+    out->bn = 256;
     out->split_k = 1;
-    out->cluster_n = ceil_div(N, 128) >= 4 && out->bn == 128 ? 4 : ceil_div(N, 128) >= 2 ? 2 : 1;
+    out->cluster_n = 1;
   } else {
     // decode: 16 (or 64) tokens per tile, K split over a cluster of up to 8 CTAs so that about two
     // CTAs per SM stream weights

@@ -33,7 +33,14 @@ namespace apt {
 
 constexpr int kTcBM = 128;       // weight rows per tile (MMA M)
 constexpr int kTcBK = 128;       // K elements per pipeline step
-constexpr int kTcAStages = 4;    // TMEM A ring depth (32 columns each)
+// TMEM A ring depth (32 columns each); decode tiles (BN = 16) fit up to 7 next to the accumulator in
+// 256 columns, so more weight steps are converted ahead of the token tile's arrival
+#ifndef APT_DEC_NACC
+#define APT_DEC_NACC 1
+#endif
+#ifndef APT_DEC_ASTAGES
+#define APT_DEC_ASTAGES 4
+#endif
 #ifdef APT_TC_TRACE
 // per-stage clock64 timeline of CTA (APT_TC_TRACE_CTA, 0) for profiling builds only
 __device__ long long g_tc_trace[8][512];
@@ -166,7 +173,8 @@ struct TcSmem {
   static constexpr int kRbOff = kWOff + kWSlots * kWBytes;       // split-K receive buffer: [S][128][cpr], cpr = ceil(BN / S), so S * cpr <= BN + S - 1 <= BN + 7
   static constexpr int kEpOff = kRbOff + (BN <= 64 ? kTcBM * (BN + 8) * 4 : 0);  // rw[128] ws[128] ra[BN] as[BN]
   static constexpr int kBarOff = kEpOff + (2 * kTcBM + 2 * BN) * 4;
-  static constexpr int kNumBars = 2 * STAGES + 2 * kWSlots + 2 * kTcAStages + 4;
+  static constexpr int kAStages = BN == 16 ? APT_DEC_ASTAGES : 4;
+  static constexpr int kNumBars = 2 * STAGES + 2 * kWSlots + 2 * kAStages + 4;
   static constexpr int kTotal = kBarOff + kNumBars * 8 + 16 + 1024;  // + tmem slot + alignment slack
 };
 
@@ -237,11 +245,15 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
   auto wfull = [&](int c) { return bars + 8u * (2 * STAGES + c); };
   auto wempty = [&](int c) { return bars + 8u * (2 * STAGES + L::kWSlots + c); };
   auto a_full = [&](int a) { return bars + 8u * (2 * STAGES + 2 * L::kWSlots + a); };
-  auto a_empty = [&](int a) { return bars + 8u * (2 * STAGES + 2 * L::kWSlots + kTcAStages + a); };
-  const uint32_t acc_full = bars + 8u * (2 * STAGES + 2 * L::kWSlots + 2 * kTcAStages);
+  auto a_empty = [&](int a) { return bars + 8u * (2 * STAGES + 2 * L::kWSlots + L::kAStages + a); };
+  const uint32_t acc_full = bars + 8u * (2 * STAGES + 2 * L::kWSlots + 2 * L::kAStages);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::kBarOff + L::kNumBars * 8);
-  constexpr uint32_t kTmemCols = (BN + 32 * kTcAStages) <= 256 ? 256 : 512;
-  constexpr uint32_t kAcol0 = BN;  // A ring after the accumulator columns
+  // decode tiles (BN = 16): the four 32-element MMAs of a K step go to four independent accumulators
+  // (summed in the epilogue), so consecutive MMAs carry no accumulator dependency and pipeline in the
+  // tensor core instead of serialising on the MMA latency
+  constexpr int kNAcc = BN == 16 ? APT_DEC_NACC : 1;
+  constexpr uint32_t kTmemCols = (BN * kNAcc + 32 * L::kAStages) <= 256 ? 256 : 512;
+  constexpr uint32_t kAcol0 = BN * kNAcc;  // A ring after the accumulator columns
   constexpr int kRowsPerCta = BN / CN;
   constexpr uint16_t kMask = (uint16_t)((1u << CN) - 1);
 
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
       mbar_init(wfull(c), 1);
       mbar_init(wempty(c), 8);      // the 8 converter warps (each reads one K step of the chunk)
     }
-    for (int a = 0; a < kTcAStages; ++a) {
+    for (int a = 0; a < L::kAStages; ++a) {
       mbar_init(a_full(a), 4);
       mbar_init(a_empty(a), 1);
     }
@@ -411,20 +423,25 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
       for (int j = 0; j < nloc; ++j) {
         const int s = L::kBAll ? j : j % STAGES;
         const uint32_t ph = (j / STAGES) & 1;
-        const int a = j % kTcAStages;
-        const uint32_t pa = (j / kTcAStages) & 1;
+        const int a = j % L::kAStages;
+        const uint32_t pa = (j / L::kAStages) & 1;
         if (!L::kBAll || j == 0) mbar_wait(full(L::kBAll ? 0 : s), L::kBAll ? 0u : ph);
         TRACE(1, j);
         if (j == 0) GTRACE(3);
+#ifndef APT_EXP_NOWAIT_A  // timing experiments only (wrong results)
         mbar_wait(a_full(a), pa);
+#endif
         TRACE(2, j);
         tc_fence_after();
         const uint64_t bdesc = umma_desc_sw128(sB + s * L::kBBytes);
+#ifndef APT_EXP_NOMMA
 #pragma unroll
         for (int kk = 0; kk < kTcBK / 32; ++kk) {
           // advance 32 K bytes inside the 128-byte swizzle atom: +2 in the (addr >> 4) field
-          tc_mma_i8(tmem, tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk), idesc, (j | kk) != 0);
+          tc_mma_i8(tmem + (uint32_t)((kk % kNAcc) * BN), tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk),
+                    idesc, (kNAcc > 1 ? (j | (kk / kNAcc)) : (j | kk)) != 0);
         }
+#endif
         if (!L::kBAll) {
           if (CN > 1) tc_commit_mc(empty(s), kMask); else tc_commit(empty(s));
         }
@@ -482,8 +499,8 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) d[8 * jj + cc] = o[cc];
       }
-      const int a = j % kTcAStages;
-      const uint32_t pa = (j / kTcAStages) & 1;
+      const int a = j % L::kAStages;
+      const uint32_t pa = (j / L::kAStages) & 1;
       if (lane == 0 && (cw & 3) == 0) TRACE(7, j);
 #ifdef APT_CONV_PIPE
       // the previous step's TMEM store completed while this step was rebuilt: publish it now
@@ -524,6 +541,16 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
     tc_fence_after();
     constexpr int kHalf = BN / 2;
     constexpr int kChunk = kHalf < 32 ? kHalf : 32;
+    auto load_acc = [&](int c0, uint32_t (&acc)[kChunk]) {
+      tmem_ld<kChunk>(tmem + lane_off + c0, acc);
+#pragma unroll
+      for (int q = 1; q < kNAcc; ++q) {
+        uint32_t t[kChunk];
+        tmem_ld<kChunk>(tmem + lane_off + (uint32_t)(q * BN) + c0, t);
+#pragma unroll
+        for (int jj = 0; jj < kChunk; ++jj) acc[jj] += t[jj];
+      }
+    };
     const int n = n0 + r;
     const int32_t rw = ep_rw[r];
     const float wsc = ep_ws[r];
@@ -531,7 +558,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
 #pragma unroll 1
       for (int c0 = par * kHalf; c0 < (par + 1) * kHalf; c0 += kChunk) {
         uint32_t acc[kChunk];
-        tmem_ld<kChunk>(tmem + lane_off + c0, acc);
+        load_acc(c0, acc);
         if (n < p.e.N) {
 #pragma unroll
           for (int jj = 0; jj < kChunk; ++jj) {
@@ -552,7 +579,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
 #pragma unroll 1
       for (int c0 = par * kHalf; c0 < (par + 1) * kHalf; c0 += kChunk) {
         uint32_t acc[kChunk];
-        tmem_ld<kChunk>(tmem + lane_off + c0, acc);
+        load_acc(c0, acc);
         if (nloc == 0) {  // an empty K range (more splits than weight chunks) contributes zero
 #pragma unroll
           for (int jj = 0; jj < kChunk; ++jj) acc[jj] = 0u;
