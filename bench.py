@@ -425,8 +425,10 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
     oracle on a bounded sample (rank 0, N=1)."""
     import torch
     res = {}
-    # ---- e2e: pinned host activations -> device, pack, GEMM, fp16 result -> pinned host
-    # one pinned staging buffer each way, so a step is 1 H2D copy, 12 packs, 36 GEMMs, 1 D2H copy
+    # ---- e2e: pinned host activations -> device, (quantize +) pack, GEMM, fp16 result -> pinned host.
+    # One pinned staging buffer each way, so a step is 1 H2D copy, 12 packs, 36 GEMMs, 1 D2H copy.
+    # "e2e" (the headline): fp16 activations through apt_quantize_pack (per-token scale = the GEMM's
+    # a_scale) -- what a quantized linear layer is fed; "e2e_codes": int8 codes through apt_pack_bipolar.
     keys = []
     for (m, wb, ab, n, k) in CASES:
         if (m, ab, k) not in keys:
@@ -435,59 +437,74 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
     for key in keys:
         a_off[key] = off
         off += key[0] * key[2]
-    h_in = torch.empty(off, dtype=torch.int8).pin_memory()
-    for key in keys:
-        m, ab, k = key
-        lo, hi = -(1 << (ab - 1)), (1 << (ab - 1))
-        h_in[a_off[key]:a_off[key] + m * k].copy_(torch.randint(lo, hi, (m * k,), dtype=torch.int8))
-    d_in = torch.empty(off, dtype=torch.int8, device=dev)
-    d_a = {key: d_in[a_off[key]:a_off[key] + key[0] * key[2]].view(key[0], key[2]) for key in keys}
-    bufs = {key: P.alloc_packed(key[0], key[2], key[1], dev, digits=True) for key in keys}
     o_shapes = [(m, shard[n]) if world == 1 else (shard[n], m) for (m, wb, ab, n, k) in CASES]
     o_total = sum(a * b for a, b in o_shapes)
     d_out_all = torch.empty(o_total, dtype=torch.float16, device=dev)
     h_out_all = torch.empty(o_total, dtype=torch.float16).pin_memory()
-    d_out, off = [], 0
+    d_out, o = [], 0
     for (a, b) in o_shapes:
-        d_out.append(d_out_all[off:off + a * b].view(a, b))
-        off += a * b
-    h2d = h_in.numel()
-    d2h = o_total * 2
-
-    def e2e_step(wset):
-        d_in.copy_(h_in, non_blocking=True)
-        for key in keys:
-            P.pack(d_a[key], key[1], out=bufs[key])
-        for i, (m, wb, ab, n, k) in enumerate(CASES):
-            P.gemm(W_packed[wset][(wb, n, k)], bufs[(m, ab, k)], out_kind="f16", layout=layout,
-                   w_scale=W_scale[(wb, n, k)], a_scale=A_scale[m], out=d_out[i], config=cfgs[i])
-        h_out_all.copy_(d_out_all, non_blocking=True)
-
-    n_e2e = max(2, min(args.steps, 50))
-    graphs = []
-    try:
-        for j in range(2):
-            gr = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gr, stream=stream):
-                e2e_step(j)
-            graphs.append(gr)
-        run = lambda j: graphs[j % 2].replay()  # noqa: E731
-    except Exception:
-        run = lambda j: e2e_step(j % 2)  # noqa: E731
-    for j in range(3):
-        run(j)
-    barrier()
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record()
-    for j in range(n_e2e):
-        run(j)
-    s1.record()
-    barrier()
-    e2e_ms = s0.elapsed_time(s1) / n_e2e
+        d_out.append(d_out_all[o:o + a * b].view(a, b))
+        o += a * b
     ops_step = sum(2 * m * n * k for (m, wb, ab, n, k) in CASES)
-    res["e2e"] = {"value": round(ops_step / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TOPS", "h2d_bytes_per_step": h2d,
-                  "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 5), "steps": n_e2e,
-                  "path": "pinned host int8 codes -> 1 H2D -> 12x apt_pack_bipolar -> 36x apt_gemm (fp16) -> 1 D2H, CUDA graph"}
+    bufs = {key: P.alloc_packed(key[0], key[2], key[1], dev, digits=True) for key in keys}
+    q_scale = {key: torch.empty(key[0], dtype=torch.float32, device=dev) for key in keys}
+
+    def e2e_leg(fp16):
+        if fp16:
+            h_in = torch.empty(off, dtype=torch.float16).pin_memory()
+            h_in.copy_(torch.randn(off, dtype=torch.float32).to(torch.float16))
+        else:
+            h_in = torch.empty(off, dtype=torch.int8).pin_memory()
+            for key in keys:
+                m, ab, k = key
+                lo, hi = -(1 << (ab - 1)), (1 << (ab - 1))
+                h_in[a_off[key]:a_off[key] + m * k].copy_(torch.randint(lo, hi, (m * k,), dtype=torch.int8))
+        d_in = torch.empty(off, dtype=h_in.dtype, device=dev)
+        d_a = {key: d_in[a_off[key]:a_off[key] + key[0] * key[2]].view(key[0], key[2]) for key in keys}
+
+        def e2e_step(wset):
+            d_in.copy_(h_in, non_blocking=True)
+            for key in keys:
+                if fp16:
+                    P.quantize_pack(d_a[key], key[1], out=bufs[key], scale=q_scale[key])
+                else:
+                    P.pack(d_a[key], key[1], out=bufs[key])
+            for i, (m, wb, ab, n, k) in enumerate(CASES):
+                P.gemm(W_packed[wset][(wb, n, k)], bufs[(m, ab, k)], out_kind="f16", layout=layout,
+                       w_scale=W_scale[(wb, n, k)], a_scale=q_scale[(m, ab, k)] if fp16 else A_scale[m],
+                       out=d_out[i], config=cfgs[i])
+            h_out_all.copy_(d_out_all, non_blocking=True)
+
+        n_e2e = max(2, min(args.steps, 50))
+        graphs = []
+        try:
+            for j in range(2):
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    e2e_step(j)
+                graphs.append(gr)
+            run = lambda j: graphs[j % 2].replay()  # noqa: E731
+        except Exception:
+            run = lambda j: e2e_step(j % 2)  # noqa: E731
+        for j in range(3):
+            run(j)
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for j in range(n_e2e):
+            run(j)
+        s1.record()
+        barrier()
+        e2e_ms = s0.elapsed_time(s1) / n_e2e
+        path = ("pinned host fp16 activations -> 1 H2D -> 12x apt_quantize_pack -> 36x apt_gemm (fp16) -> 1 D2H"
+                if fp16 else "pinned host int8 codes -> 1 H2D -> 12x apt_pack_bipolar -> 36x apt_gemm (fp16) -> 1 D2H")
+        return {"value": round(ops_step / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TOPS",
+                "h2d_bytes_per_step": h_in.numel() * h_in.element_size(), "d2h_bytes_per_step": o_total * 2,
+                "ms_per_step": round(e2e_ms, 5), "steps": n_e2e, "path": path + ", CUDA graph"}
+
+    res["e2e"] = e2e_leg(True)
+    res["e2e_codes"] = e2e_leg(False)
+    n_e2e = res["e2e"]["steps"]
 
     # ---- cuBLAS FP16 and INT8 on the same 36 cases (dense weights, 2 alternating sets)
     if world == 1:

@@ -305,16 +305,18 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
   };
   const int n_pre = min(L::kWSlots, (nloc + 1) / 2);
   const int pre_s0 = min(2, min(nloc, 2 * n_pre));  // steps in the first prefetch run
-  auto issue_pre = [&]() {
+  // part: 1 = first run only, 2 = the rest only, 3 = both
+  auto issue_pre = [&](int part) {
     if (tiled) {
       // the first ring's worth of steps in two runs per plane: chunk 0 (conversion starts as soon as
       // it lands) and the rest
       const int pre = min(nloc, 2 * n_pre);
       const int s0 = pre_s0;
-      if (s0 > 0) {
+      if ((part & 1) && s0 > 0) {
         mbar_expect_tx(wbig0, (uint32_t)(s0 * 2048 * WB));
         w_run(0, s0, 0, wbig0);
       }
+      if (!(part & 2)) return;
       if (pre > s0) {
         mbar_expect_tx(wbig, (uint32_t)((pre - s0) * 2048 * WB));
         w_run(s0, pre - s0, s0 / 2, wbig);
@@ -323,9 +325,18 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
       // slot's second use (chunk c + kWSlots) is its phase 1
       for (int c = 0; c < n_pre; ++c) mbar_arrive(wfull(c));
     } else {
-      for (int c = 0; c < n_pre; ++c) issue_w(c);
+      if (part & 2)
+        for (int c = 0; c < n_pre; ++c) issue_w(c);
     }
   };
+  // decode tiles: only the first weight run goes out before griddepcontrol.wait; the token slab is
+  // requested right after the wait, ahead of the rest of the weight prefetch (else it queues behind
+  // ~64 KB of weight copies per CTA and the MMA idles ~0.6 us)
+#ifdef APT_DEC_TOK_EARLY
+  constexpr bool kTokEarly = L::kBAll && CN == 1;
+#else
+  constexpr bool kTokEarly = false;
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
     // but this thread's barriers: the first ring's worth of chunks is requested before the rest of
     // the setup (TMEM allocation, CTA / cluster barriers)
 #ifndef APT_TC_LATE_W
-    if (CN == 1) issue_pre();
+    if (CN == 1) issue_pre(kTokEarly && tiled ? 1 : 3);
 #endif
     GTRACE(8);
   }
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
 #ifndef APT_TC_LATE_W
       if (CN > 1)
 #endif
-        issue_pre();
+        issue_pre(3);
       pdl_wait();
       GTRACE(15);
       if constexpr (L::kBAll) {
@@ -394,6 +405,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
         // ahead of the weight prefetch measured 5% slower in back-to-back launches.)
         mbar_expect_tx(full(0), (uint32_t)(nloc * L::kBBytes));
         for (int j = 0; j < nloc; ++j) tma_load_2d(sB + j * L::kBBytes, &tm_b, full(0), (kb + j) * kTcBK, m0);
+        if (kTokEarly && tiled) issue_pre(2);
       }
       for (int j = 0; j < nloc; ++j) {
         const int ks = kb + j;
