@@ -65,6 +65,15 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def kernel_mix(cfgs):
+    """Launch count per kernel family of one GEMM phase (from the selector's configs)."""
+    names = {1: "gemm_mma_kernel (mma.sync)", 2: "gemm_tc_kernel (tcgen05)", 3: "gemv_kernel (SIMT dp4a)"}
+    mix = {}
+    for c in cfgs:
+        mix[names[c["kernel"]]] = mix.get(names[c["kernel"]], 0) + 1
+    return mix
+
+
 def load_traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "decode_traffic.json")) as f:
@@ -349,7 +358,8 @@ def main():
                        "parallelism": f"tp{world} (N-split + all-gather)" if world > 1 else "single GPU",
                        "cuda_graphs": use_graphs},
             "gpu_launches": (len(A_codes) + len(CASES)) * args.steps,
-            "roofline": {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 bit-plane GEMM, 36 launches/step)",
+            "roofline": {"bound": "hbm", "kernel": "decode GEMM phase: " + ", ".join(
+                             f"{k} x{v}" for k, v in sorted(kernel_mix(cfgs).items())) + " launches/step",
                          "measured": "GEMM phase of every timed step (events around the graph of 36 GEMM launches"
                                      + (" + all-gathers" if world > 1 else "") + ")",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",

@@ -156,8 +156,11 @@ typedef enum {
   APT_KERNEL_AUTO = 0,
   APT_KERNEL_MMA_SPLITK = 1, /* register-rebuild mma.sync u8 kernel, split-K reduced in a thread-block
                                 cluster through distributed shared memory (decode / small M)     */
-  APT_KERNEL_TC = 2          /* tcgen05 kind::i8 kernel: weights rebuilt in registers -> TMEM (A operand),
+  APT_KERNEL_TC = 2,         /* tcgen05 kind::i8 kernel: weights rebuilt in registers -> TMEM (A operand),
                                 tokens via TMA from the int8 token workspace, s32 accumulator in TMEM */
+  APT_KERNEL_GEMV = 3        /* M <= 4: SIMT GEMV, weights rebuilt in registers (same u8 digits), dp4a
+                                against the activation digit view; 32 weight rows x all of K per CTA
+                                (bm = 32, bn = M, bk = 128, split_k = 8 warps, stages = 1)        */
 } apt_kernel;
 
 /* Kernel configuration (the B200 analogue of the paper's tunable hyperparameters, §5.1).

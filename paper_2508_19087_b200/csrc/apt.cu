@@ -45,6 +45,13 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
     if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
     return APT_OK;
   }
+  if (c->kernel == APT_KERNEL_GEMV) {
+    if (M > 4 || c->bm != 32 || c->bn != M || c->bk != 128 || (c->split_k != 8 && c->split_k != 16) ||
+        c->stages != 1)
+      return APT_ERR_UNSUPPORTED;
+    if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
+    return APT_OK;
+  }
   if (c->kernel == APT_KERNEL_TC) {
     if (c->bm != 128 || c->bk != 128) return APT_ERR_UNSUPPORTED;
     if (c->bn != 16 && c->bn != 64 && c->bn != 128 && c->bn != 256) return APT_ERR_UNSUPPORTED;
@@ -164,6 +171,17 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
     out->bn = 256;
     out->split_k = 1;
     out->cluster_n = 1;
+  } else if (M <= 2) {
+    // one or two tokens: the SIMT dp4a GEMV (SURVEY §8 a9 "pick by measurement"; 1.2-2.2x faster
+    // than the tensor-core decode tile on every Llama-2-7B decode linear at M = 1, 2).
+    // 16 warps per 32-row CTA when the row tiles do not fill the SMs, else 8 warps, 3 CTAs per SM.
+    out->kernel = APT_KERNEL_GEMV;
+    out->bm = 32;
+    out->bn = M;
+    out->split_k = ceil_div(N, 32) <= kNumSMs ? 16 : 8;
+    out->cluster_n = 1;
+    out->stages = 1;
+    return APT_OK;
   } else {
     // decode: 16 (or 64) tokens per tile, K split over a cluster of up to 8 CTAs so that about two
     // CTAs per SM stream weights
@@ -188,7 +206,7 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
 size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
   // TC kernel: activation digit view for activations packed without one (apt_packed.digits == NULL)
   (void)N;
-  if (!cfg || M <= 0 || K <= 0 || cfg->kernel != APT_KERNEL_TC) return 0;
+  if (!cfg || M <= 0 || K <= 0 || (cfg->kernel != APT_KERNEL_TC && cfg->kernel != APT_KERNEL_GEMV)) return 0;
   return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
 }
 
@@ -217,7 +235,7 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   }
   st = validate_config(&c, M, N, K, wbits, abits);
   if (st != APT_OK) return st;
-  const size_t need = (A->digits && c.kernel == APT_KERNEL_TC) ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
+  const size_t need = (A->digits && c.kernel != APT_KERNEL_MMA_SPLITK) ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
   if (need > 0 && (!workspace || ws_bytes < need || !aligned16(workspace))) return APT_ERR_WORKSPACE;
   if (A->digits && !aligned16(A->digits)) return APT_ERR_INVALID_ARGUMENT;
 
@@ -259,6 +277,17 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
                                                 reinterpret_cast<uint8_t*>(workspace), s);
     if (err != cudaSuccess) return APT_ERR_CUDA;
     adig = reinterpret_cast<const uint8_t*>(workspace);
+  }
+  if (c.kernel == APT_KERNEL_GEMV) {
+    apt::GemvArgs p;
+    p.wp = W->planes;
+    p.w_tiled = W->layout == APT_PACK_TILED ? 1 : 0;
+    p.w_pstride = (int64_t)(p.w_tiled ? (N + 127) / 128 * 128 : N) * W->k_words;
+    p.adig = adig;
+    p.k_words = W->k_words;
+    p.e = e;
+    cudaError_t err = apt::launch_gemv(p, wbits, c.split_k, s);
+    return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   if (c.kernel == APT_KERNEL_TC) {
     apt::TcArgs p;

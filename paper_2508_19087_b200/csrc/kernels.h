@@ -53,3 +53,16 @@ cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, in
 int tc_stages(int wbits, int bn);
 size_t tc_workspace_bytes(int M, int k_words);
 }  // namespace apt
+
+namespace apt {
+struct GemvArgs {
+  const uint32_t* wp;      // weight planes (row or tile-major layout)
+  int64_t w_pstride;       // words per plane
+  int32_t w_tiled;
+  const uint8_t* adig;     // activation digits [M][Kpad], kernel K order
+  int32_t k_words;
+  EpilogueArgs e;
+};
+// M <= 4 tokens: SIMT dp4a GEMV over rebuilt weight digits (gemv.cu)
+cudaError_t launch_gemv(const GemvArgs& p, int wbits, int warps, cudaStream_t stream);  // warps: 8 or 16
+}  // namespace apt

@@ -65,8 +65,11 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab):
     if c.kernel == L.APT_KERNEL_MMA_SPLITK:
         assert c.bm == 32 and c.bn in (8, 16) and c.bn >= min(M, 16)
         assert c.split_k == 4 and c.cluster_n == 1
+    elif c.kernel == L.APT_KERNEL_GEMV:
+        assert M <= 2 and c.bm == 32 and c.bn == M and c.split_k in (8, 16) and c.stages == 1
+        assert c.cluster_n == 1 and c.cta_pair == 0
     else:
-        assert c.kernel == L.APT_KERNEL_TC
+        assert c.kernel == L.APT_KERNEL_TC and M > 2
         assert c.bm == 128 and c.bn in (16, 64, 128, 256) and c.cluster_n in (1, 2, 4)
         assert 1 <= c.split_k <= 8 and c.cluster_n * c.split_k <= 8
         assert c.bn >= min(M, 128 if M > 64 else 64)

@@ -336,3 +336,58 @@ def test_quantize_pack_then_gemm_f16(m, pa, pw):
     codes, so = O.quantize_symmetric(x, pa)
     ref = O.scale_fp64(O.gemm_signed(codes, w), ws, so)
     assert (np.abs(got - ref) <= 1e-3 * np.abs(ref) + 2.0 ** -24).all()
+
+
+# ----------------------------------------------------------------------------- SIMT GEMV (M <= 4)
+
+def _gemv_cfg(m, n, k, wb, ab, warps=8):
+    return dict(P.select_config(m, n, k, wb, ab), kernel=3, bm=32, bn=m, bk=128, split_k=warps, stages=1,
+                cta_pair=0, cluster_n=1)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4])
+@pytest.mark.parametrize("pw,pa", [(1, 1), (1, 2), (2, 2), (3, 4), (4, 4), (5, 3), (8, 8), (7, 1)])
+@pytest.mark.parametrize("tiled", [True, False])
+@pytest.mark.parametrize("warps", [8, 16])
+def test_gemv_matches_oracle(m, pw, pa, tiled, warps):
+    """APT_KERNEL_GEMV: int32 signed and bipolar bit-exact, fp16 within 1e-3, on a ragged shape
+    (N not a multiple of 32 or 128, K not a multiple of 256, fewer K steps than warps)."""
+    for n, k in ((333, 700), (100, 64)):
+        a = signed_codes(m, k, pa, seed=50 + m + pa)
+        w = signed_codes(n, k, pw, seed=60 + pw + n)
+        A = P.pack(_dev(a), pa, digits=True)
+        W = P.pack(_dev(w), pw, tiled=tiled)
+        cfg = _gemv_cfg(m, n, k, pw, pa, warps)
+        ref = O.gemm_signed(a, w)
+        assert np.array_equal(P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64), ref)
+        got = P.gemm(W, A, out_kind="bipolar", layout="col", config=cfg).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got.T, O.gemm_bipolar(a, pa, w, pw))
+        ws = log_uniform_scales(n, -10, -6, seed=3)
+        as_ = log_uniform_scales(m, -6, -2, seed=4)
+        got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_), config=cfg).cpu().numpy()
+        r = O.scale_fp64(ref, ws, as_)
+        assert (np.abs(got.astype(np.float64) - r) <= 1e-3 * np.abs(r) + 2.0 ** -24).all()
+
+
+def test_gemv_without_digit_view():
+    """Activations packed without the digit view: the GEMV reads the workspace expansion."""
+    m, n, k = 1, 256, 4096
+    a = signed_codes(m, k, 4, seed=1)
+    w = signed_codes(n, k, 3, seed=2)
+    A = P.pack(_dev(a), 4)
+    W = P.pack(_dev(w), 3, tiled=True)
+    got = P.gemm(W, A, config=_gemv_cfg(m, n, k, 3, 4)).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, O.gemm_signed(a, w))
+
+
+@pytest.mark.parametrize("n,k", LLAMA7B)
+@pytest.mark.parametrize("pw,pa", [(1, 2), (2, 2), (3, 4), (4, 4)])
+def test_gemv_llama7b_full(n, k, pw, pa):
+    """BASELINE configs[1] at M = 1 through the GEMV, every element vs the C oracle."""
+    a = signed_codes(1, k, pa, seed=config_seed(1, pw, pa, salt=3))
+    w = signed_codes(n, k, pw, seed=config_seed(1, pw, pa, salt=3) + 1)
+    A, W = _pack_both(a, pa, w, pw)
+    cfg = P.select_config(1, n, k, pw, pa)
+    assert cfg["kernel"] == 3  # the selector's M = 1 choice, in its launch configuration
+    got = P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, c_gemm_i64(a, w))
