@@ -171,7 +171,7 @@ typedef enum {
  *   bn       : tokens per CTA tile (MMA N side)
  *   bk       : K elements per pipeline step
  *   stages   : pipeline depth (TC kernel)
- *   split_k  : K splits (MMA_SPLITK kernel: the cluster size, 1..8)
+ *   split_k  : K splits (MMA_SPLITK / TC kernels: the cluster size, 1..8; GEMV: warps per CTA, 8 or 16)
  *   cta_pair : 1 = cta_group::2 pairs (TC kernel), 0 = single CTA (this build: 0)
  *   cluster_n: TC kernel: CTAs along N (weight tiles) sharing one token tile; the token tile is loaded
  *              once per cluster with TMA multicast (1, 2 or 4)                                          */
@@ -180,7 +180,11 @@ typedef struct {
 } apt_config;
 
 /* Host, pure and deterministic (replaces the paper's lookup table + search, §5.2).
- * p = wbits, q = abits as in the north_star's "W_p x A_q".
+ * p = wbits, q = abits as in the north_star's "W_p x A_q".  Rules (measured on B200):
+ *   M <= 2       -> APT_KERNEL_GEMV, 16 warps per CTA if ceil(N/32) <= 148 else 8;
+ *   M <= 64      -> APT_KERNEL_TC decode tile (bn 16 for M <= 16 else 64), K split over a cluster so that
+ *                   about two CTAs per SM stream weights (<= 16 K steps per CTA at bn 16);
+ *   M > 64       -> APT_KERNEL_TC, bn 256, one CTA per SM, no cluster.
  * Errors: APT_ERR_INVALID_ARGUMENT (dims <= 0, bits outside [1,8], null out),
  *         APT_ERR_UNSUPPORTED (int32 bound, reading Q8). */
 APT_API apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits,

@@ -391,3 +391,47 @@ def test_gemv_llama7b_full(n, k, pw, pa):
     assert cfg["kernel"] == 3  # the selector's M = 1 choice, in its launch configuration
     got = P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64)
     assert np.array_equal(got, c_gemm_i64(a, w))
+
+
+# ----------------------------------------------------------------------------- configs[3], configs[4] at full size
+
+def _sampled_check(got, a, w, rows):
+    assert np.array_equal(got[rows], c_gemm_i64(a[rows], w))
+    wsum = w.astype(np.int64).sum(0)
+    assert np.array_equal(got.sum(1), a.astype(np.int64) @ wsum)
+
+
+@pytest.mark.parametrize("n,k", [(8192, 8192), (28672, 8192)])
+def test_llama70b_sampled_and_tp_slices(n, k):
+    """BASELINE configs[3] (Llama-3-70B linears, M = 4096, W2A4) at full size in the selector's launch
+    configuration: 8 sampled token rows vs the C oracle, the row-sum identity over all rows, and the
+    N-split tensor-parallel slices (P = 8, column layout, as each rank computes them) concatenate to
+    the single-GPU result bit for bit."""
+    m, pw, pa = 4096, 2, 4
+    a = signed_codes(m, k, pa, seed=config_seed(3, pw, pa))
+    w = signed_codes(n, k, pw, seed=config_seed(3, pw, pa) + 1)
+    A, W = _pack_both(a, pa, w, pw)
+    full = P.gemm(W, A)
+    got = full.cpu().numpy().astype(np.int64)
+    _sampled_check(got, a, w, np.random.default_rng(3).choice(m, 8, replace=False))
+    p = 8
+    rows = n // p
+    for r in (0, p - 1):
+        Wr = P.pack(_dev(w[r * rows:(r + 1) * rows]), pw, tiled=True)
+        yt = P.gemm(Wr, A, layout="col")  # [rows, M] = the rank's block of Y^T
+        assert torch.equal(yt.t(), full[:, r * rows:(r + 1) * rows])
+
+
+@pytest.mark.parametrize("pw", range(1, 9))
+def test_sweep_4096_cube_sampled(pw):
+    """BASELINE configs[4]: 4096^3 for every (p_w, p_a) in 1..8 x 1..8 with the selector's config,
+    4 sampled token rows vs the C oracle plus the row-sum identity."""
+    n = m = k = 4096
+    w = signed_codes(n, k, pw, seed=config_seed(4, pw, 0))
+    W = P.pack(_dev(w), pw, tiled=True)
+    rows = np.random.default_rng(pw).choice(m, 4, replace=False)
+    for pa in range(1, 9):
+        a = signed_codes(m, k, pa, seed=config_seed(4, pw, pa))
+        A = P.pack(_dev(a), pa, digits=True)
+        got = P.gemm(W, A).cpu().numpy().astype(np.int64)
+        _sampled_check(got, a, w, rows)
