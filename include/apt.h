@@ -158,9 +158,13 @@ typedef enum {
                                 cluster through distributed shared memory (decode / small M)     */
   APT_KERNEL_TC = 2,         /* tcgen05 kind::i8 kernel: weights rebuilt in registers -> TMEM (A operand),
                                 tokens via TMA from the int8 token workspace, s32 accumulator in TMEM */
-  APT_KERNEL_GEMV = 3        /* M <= 4: SIMT GEMV, weights rebuilt in registers (same u8 digits), dp4a
+  APT_KERNEL_GEMV = 3,       /* M <= 4: SIMT GEMV, weights rebuilt in registers (same u8 digits), dp4a
                                 against the activation digit view; 32 weight rows x all of K per CTA
-                                (bm = 32, bn = M, bk = 128, split_k = 8 warps, stages = 1)        */
+                                (bm = 32, bn = M, bk = 128, split_k = 8 or 16 warps, stages = 1)  */
+  APT_KERNEL_SKINNY = 4      /* M <= 16 per token tile: mma.sync m16n8k32 u8 fed from registers (weights
+                                rebuilt in registers, tokens from the digit view), 16 weight rows x
+                                bn (8 or 16) tokens x all of K per CTA (bm = 16, bk = 256,
+                                split_k = 4, 8 or 16 warps splitting K, stages = 1)                */
 } apt_kernel;
 
 /* Kernel configuration (the B200 analogue of the paper's tunable hyperparameters, §5.1).
@@ -182,6 +186,7 @@ typedef struct {
 /* Host, pure and deterministic (replaces the paper's lookup table + search, §5.2).
  * p = wbits, q = abits as in the north_star's "W_p x A_q".  Rules (measured on B200):
  *   M <= 2       -> APT_KERNEL_GEMV, 16 warps per CTA if ceil(N/32) <= 148 else 8;
+ *   M <= 8, K <= 4096 -> APT_KERNEL_SKINNY, bn 8, 8 warps per CTA if ceil(N/16) <= 296 else 4;
  *   M <= 64      -> APT_KERNEL_TC decode tile (bn 16 for M <= 16 else 64), K split over a cluster so that
  *                   about two CTAs per SM stream weights (<= 16 K steps per CTA at bn 16);
  *   M > 64       -> APT_KERNEL_TC, bn 256, one CTA per SM, no cluster.

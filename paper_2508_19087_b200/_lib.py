@@ -14,7 +14,7 @@ APT_OK, APT_ERR_INVALID_ARGUMENT, APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ER
 APT_ENC_SIGNED, APT_ENC_BIPOLAR = 0, 1
 APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
 APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
-APT_KERNEL_AUTO, APT_KERNEL_MMA_SPLITK, APT_KERNEL_TC, APT_KERNEL_GEMV = 0, 1, 2, 3
+APT_KERNEL_AUTO, APT_KERNEL_MMA_SPLITK, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY = 0, 1, 2, 3, 4
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes",

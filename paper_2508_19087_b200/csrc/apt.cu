@@ -52,6 +52,12 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
     if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
     return APT_OK;
   }
+  if (c->kernel == APT_KERNEL_SKINNY) {
+    if (c->bm != 16 || (c->bn != 8 && c->bn != 16) || c->bk != 256 || c->stages != 1) return APT_ERR_UNSUPPORTED;
+    if (c->split_k != 4 && c->split_k != 8 && c->split_k != 16) return APT_ERR_UNSUPPORTED;
+    if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
+    return APT_OK;
+  }
   if (c->kernel == APT_KERNEL_TC) {
     if (c->bm != 128 || c->bk != 128) return APT_ERR_UNSUPPORTED;
     if (c->bn != 16 && c->bn != 64 && c->bn != 128 && c->bn != 256) return APT_ERR_UNSUPPORTED;
@@ -182,6 +188,19 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
     out->cluster_n = 1;
     out->stages = 1;
     return APT_OK;
+  } else if (M <= 8 && K <= 4096) {
+    // up to 8 tokens, K <= 4096: the mma.sync skinny GEMM fed from registers (1.07-1.48x faster than
+    // the tcgen05 tile at M = 8 on 4096x4096 and 11008x4096; slower at K = 11008 and at M = 16,
+    // profiles/r1_skinny_vs_tc.txt).  8 warps per 16-row CTA while the row tiles fit twice on the
+    // SMs, else 4.
+    out->kernel = APT_KERNEL_SKINNY;
+    out->bm = 16;
+    out->bn = 8;
+    out->bk = 256;
+    out->split_k = ceil_div(N, 16) <= 2 * kNumSMs ? 8 : 4;
+    out->cluster_n = 1;
+    out->stages = 1;
+    return APT_OK;
   } else {
     // decode: 16 (or 64) tokens per tile, K split over a cluster of up to 8 CTAs so that about two
     // CTAs per SM stream weights
@@ -206,7 +225,7 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
 size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
   // TC kernel: activation digit view for activations packed without one (apt_packed.digits == NULL)
   (void)N;
-  if (!cfg || M <= 0 || K <= 0 || (cfg->kernel != APT_KERNEL_TC && cfg->kernel != APT_KERNEL_GEMV)) return 0;
+  if (!cfg || M <= 0 || K <= 0 || cfg->kernel == APT_KERNEL_MMA_SPLITK) return 0;
   return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
 }
 
@@ -278,7 +297,7 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
     if (err != cudaSuccess) return APT_ERR_CUDA;
     adig = reinterpret_cast<const uint8_t*>(workspace);
   }
-  if (c.kernel == APT_KERNEL_GEMV) {
+  if (c.kernel == APT_KERNEL_GEMV || c.kernel == APT_KERNEL_SKINNY) {
     apt::GemvArgs p;
     p.wp = W->planes;
     p.w_tiled = W->layout == APT_PACK_TILED ? 1 : 0;
@@ -286,7 +305,8 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
     p.adig = adig;
     p.k_words = W->k_words;
     p.e = e;
-    cudaError_t err = apt::launch_gemv(p, wbits, c.split_k, s);
+    cudaError_t err = c.kernel == APT_KERNEL_GEMV ? apt::launch_gemv(p, wbits, c.split_k, s)
+                                                  : apt::launch_gemm_skinny(p, wbits, c.bn, c.split_k, s);
     return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   if (c.kernel == APT_KERNEL_TC) {

@@ -65,4 +65,6 @@ struct GemvArgs {
 };
 // M <= 4 tokens: SIMT dp4a GEMV over rebuilt weight digits (gemv.cu)
 cudaError_t launch_gemv(const GemvArgs& p, int wbits, int warps, cudaStream_t stream);  // warps: 8 or 16
+// M <= 16: mma.sync m16n8k32 u8 skinny GEMM fed from registers (gemm_skinny.cu); bn 8 or 16, warps 4/8/16
+cudaError_t launch_gemm_skinny(const GemvArgs& p, int wbits, int bn, int warps, cudaStream_t stream);
 }  // namespace apt

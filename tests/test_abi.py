@@ -52,7 +52,7 @@ def _select(M, N, K, wb, ab):
     return rc, c
 
 
-@pytest.mark.parametrize("M", [1, 8, 16, 64, 2048])
+@pytest.mark.parametrize("M", [1, 2, 3, 8, 16, 64, 2048])
 @pytest.mark.parametrize("N,K", [(4096, 4096), (11008, 4096), (4096, 11008), (256, 256), (7, 1)])
 @pytest.mark.parametrize("wb,ab", [(1, 2), (2, 2), (3, 4), (4, 4), (8, 8)])
 def test_selector_legal_and_deterministic(M, N, K, wb, ab):
@@ -68,6 +68,9 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab):
     elif c.kernel == L.APT_KERNEL_GEMV:
         assert M <= 2 and c.bm == 32 and c.bn == M and c.split_k in (8, 16) and c.stages == 1
         assert c.cluster_n == 1 and c.cta_pair == 0
+    elif c.kernel == L.APT_KERNEL_SKINNY:
+        assert 2 < M <= 8 and K <= 4096 and c.bm == 16 and c.bn == 8 and c.bk == 256
+        assert c.split_k in (4, 8) and c.stages == 1 and c.cluster_n == 1 and c.cta_pair == 0
     else:
         assert c.kernel == L.APT_KERNEL_TC and M > 2
         assert c.bm == 128 and c.bn in (16, 64, 128, 256) and c.cluster_n in (1, 2, 4)

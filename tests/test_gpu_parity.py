@@ -435,3 +435,45 @@ def test_sweep_4096_cube_sampled(pw):
         A = P.pack(_dev(a), pa, digits=True)
         got = P.gemm(W, A).cpu().numpy().astype(np.int64)
         _sampled_check(got, a, w, rows)
+
+
+# ----------------------------------------------------------------------------- mma.sync skinny GEMM (M <= 16)
+
+def _skinny_cfg(m, n, k, wb, ab, bn=16, warps=8):
+    return dict(P.select_config(m, n, k, wb, ab), kernel=4, bm=16, bn=bn, bk=256, split_k=warps, stages=1,
+                cta_pair=0, cluster_n=1)
+
+
+@pytest.mark.parametrize("m,bn", [(1, 8), (5, 8), (8, 8), (9, 16), (16, 16), (16, 8), (21, 16)])
+@pytest.mark.parametrize("pw,pa", [(1, 1), (1, 2), (2, 2), (3, 4), (4, 4), (6, 5), (8, 8)])
+@pytest.mark.parametrize("warps", [4, 8, 16])
+def test_skinny_matches_oracle(m, bn, pw, pa, warps):
+    """APT_KERNEL_SKINNY: int32 signed / bipolar bit-exact and fp16 within 1e-3 on ragged shapes
+    (N not a multiple of 16, K not a multiple of 256, fewer iterations than warps, M > bn -> 2 tiles),
+    tile-major and canonical weights."""
+    for n, k, tiled in ((333, 700, True), (100, 64, False), (40, 1300, True)):
+        a = signed_codes(m, k, pa, seed=70 + m + pa)
+        w = signed_codes(n, k, pw, seed=80 + pw + n)
+        A = P.pack(_dev(a), pa, digits=True)
+        W = P.pack(_dev(w), pw, tiled=tiled)
+        cfg = _skinny_cfg(m, n, k, pw, pa, bn, warps)
+        ref = O.gemm_signed(a, w)
+        assert np.array_equal(P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64), ref)
+        got = P.gemm(W, A, out_kind="bipolar", layout="col", config=cfg).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got.T, O.gemm_bipolar(a, pa, w, pw))
+        ws = log_uniform_scales(n, -10, -6, seed=5)
+        as_ = log_uniform_scales(m, -6, -2, seed=6)
+        got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_), config=cfg).cpu().numpy()
+        r = O.scale_fp64(ref, ws, as_)
+        assert (np.abs(got.astype(np.float64) - r) <= 1e-3 * np.abs(r) + 2.0 ** -24).all()
+
+
+@pytest.mark.parametrize("n,k", LLAMA7B)
+@pytest.mark.parametrize("m", [8, 16])
+@pytest.mark.parametrize("pw,pa", [(1, 2), (4, 4)])
+def test_skinny_llama7b_full(n, k, m, pw, pa):
+    a = signed_codes(m, k, pa, seed=config_seed(1, pw, pa, salt=5))
+    w = signed_codes(n, k, pw, seed=config_seed(1, pw, pa, salt=5) + 1)
+    A, W = _pack_both(a, pa, w, pw)
+    got = P.gemm(W, A, config=_skinny_cfg(m, n, k, pw, pa, bn=8 if m <= 8 else 16)).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, c_gemm_i64(a, w))

@@ -57,8 +57,9 @@ def case(m, n, k, wb, ab, cfg=None, baselines=True, tag=""):
     dev = torch.device("cuda")
     wbytes = n * kpad(k) * wb // 8
     copies = max(1, min(16, -(-2 * L2_BYTES // max(wbytes, 1))))
-    Ws = [P.pack(torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev), wb, tiled=True)
-          for _ in range(copies)]
+    tiled = (cfg or {}).get("kernel", 2) != 1  # the mma.sync kernel reads canonical planes
+    Ws = [P.pack(torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev), wb,
+                 tiled=tiled) for _ in range(copies)]
     a = torch.randint(-(1 << (ab - 1)), 1 << (ab - 1), (m, k), dtype=torch.int8, device=dev)
     A = P.pack(a, ab, digits=True)
     ws = torch.rand(n, device=dev) * 1e-3
