@@ -67,7 +67,8 @@ def load_peaks():
 
 def kernel_mix(cfgs):
     """Launch count per kernel family of one GEMM phase (from the selector's configs)."""
-    names = {1: "gemm_mma_kernel (mma.sync)", 2: "gemm_tc_kernel (tcgen05)", 3: "gemv_kernel (SIMT dp4a)"}
+    names = {1: "gemm_mma_kernel (mma.sync)", 2: "gemm_tc_kernel (tcgen05)", 3: "gemv_kernel (SIMT dp4a)",
+             4: "gemm_skinny_kernel (mma.sync from registers)"}
     mix = {}
     for c in cfgs:
         mix[names[c["kernel"]]] = mix.get(names[c["kernel"]], 0) + 1

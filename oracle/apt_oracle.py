@@ -278,3 +278,17 @@ def quantize_symmetric(x: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray]:
         q = np.rint(x32[r] / s)              # fp32 division, then half-to-even
         codes[r] = np.clip(q, lo, hi).astype(np.int8)
     return codes, scales
+
+
+def dequant_gemm_fp64(a_codes: np.ndarray, w_codes: np.ndarray, w_scale, a_scale, w_zero=None,
+                      a_zero=None) -> np.ndarray:
+    """P:199-201 linear quantization with zero points on both operands, the plain
+    definition: dequantize X = a_scale x_hat + a_zero and W = w_scale w_hat + w_zero in fp64, then
+    out = X . W^T (fp64 matmul).  Scales / zeros are fp32 arrays (or None: scale 1, zero 0)."""
+    m, k = a_codes.shape
+    n = w_codes.shape[0]
+    def vec(v, size, default):
+        return np.full(size, default, dtype=np.float64) if v is None else np.asarray(v, dtype=np.float64)
+    X = vec(a_scale, m, 1.0)[:, None] * a_codes.astype(np.float64) + vec(a_zero, m, 0.0)[:, None]
+    W = vec(w_scale, n, 1.0)[:, None] * w_codes.astype(np.float64) + vec(w_zero, n, 0.0)[:, None]
+    return X @ W.T

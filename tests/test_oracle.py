@@ -354,3 +354,23 @@ def test_quantize_power_of_two_invariance():
     c1, s1 = O.quantize_symmetric(x, 4)
     c2, s2 = O.quantize_symmetric((x.astype(np.float32) * 8).astype(np.float16), 4)
     assert np.array_equal(c1, c2) and np.array_equal(s2, s1 * 8)
+
+
+def test_dequant_gemm_exact_brute_force():
+    """dequant_gemm_fp64 vs exact rational brute force sum_k (s_a x + z_a)(s_w w + z_w) on tiny inputs
+    (pins the zero-point definition of), and the zero-free case equals scale_fp64."""
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        m, n, k = rng.integers(1, 5, size=3)
+        a = signed_codes(m, k, 4, seed=int(rng.integers(1 << 30)))
+        w = signed_codes(n, k, 3, seed=int(rng.integers(1 << 30)))
+        ws, as_ = rng.uniform(0.01, 1, n).astype(np.float32), rng.uniform(0.01, 1, m).astype(np.float32)
+        wz, az = rng.uniform(-1, 1, n).astype(np.float32), rng.uniform(-1, 1, m).astype(np.float32)
+        got = O.dequant_gemm_fp64(a, w, ws, as_, wz, az)
+        for i in range(m):
+            for j in range(n):
+                ex = sum((Fraction(float(as_[i])) * int(a[i, q]) + Fraction(float(az[i]))) *
+                         (Fraction(float(ws[j])) * int(w[j, q]) + Fraction(float(wz[j]))) for q in range(k))
+                assert abs(Fraction(got[i, j]) - ex) <= Fraction(1, 1 << 40) * (1 + abs(ex))
+        assert np.allclose(O.dequant_gemm_fp64(a, w, ws, as_), O.scale_fp64(O.gemm_signed(a, w), ws, as_),
+                           rtol=1e-14, atol=0)
