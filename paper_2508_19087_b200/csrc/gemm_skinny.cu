@@ -48,7 +48,18 @@ template <int WB, int NT, int NW>
 __global__ void __launch_bounds__(32 * NW, SkShape<NW>::kMinBlocks) gemm_skinny_kernel(GemvArgs p) {
   constexpr int BN = 8 * NT;
   // iterations whose weight loads are in flight together (double-buffered)
+#ifdef APT_SK_BATCH
+  constexpr int kBatch = APT_SK_BATCH;
+#else
   constexpr int kBatch = WB <= 2 ? 2 : 1;
+#endif
+  // independent accumulator chains per 8-token tile (consecutive mma.sync into one accumulator
+  // serialise on the MMA latency)
+#ifdef APT_SK_ACC
+  constexpr int kAcc = APT_SK_ACC;
+#else
+  constexpr int kAcc = 1;
+#endif
   pdl_launch_dependents();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -76,11 +87,13 @@ __global__ void __launch_bounds__(32 * NW, SkShape<NW>::kMinBlocks) gemm_skinny_
         }
       }
   };
-  int c[NT][4];
+  int c[NT][kAcc][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) c[nt][j] = 0;
+    for (int q = 0; q < kAcc; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[nt][q][j] = 0;
   load_batch(i0);
   pdl_wait();  // activation digits, row sums and scales may come from the previous kernel
   // this lane's token rows (one per 8-token tile), clamped: columns >= M are never stored
@@ -119,7 +132,8 @@ __global__ void __launch_bounds__(32 * NW, SkShape<NW>::kMinBlocks) gemm_skinny_
           const uint32_t d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
           for (int s = 0; s < 4; ++s)
-            mma_u8_16816(c[nt], oa[2 * s], ob[2 * s], oa[2 * s + 1], ob[2 * s + 1], d[2 * s], d[2 * s + 1]);
+            mma_u8_16816(c[nt][(grp * 4 + s) % kAcc], oa[2 * s], ob[2 * s], oa[2 * s + 1], ob[2 * s + 1], d[2 * s],
+                         d[2 * s + 1]);
         }
       }
     }
@@ -128,10 +142,17 @@ __global__ void __launch_bounds__(32 * NW, SkShape<NW>::kMinBlocks) gemm_skinny_
   __shared__ int32_t red[NW][kSkRows][BN];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    red[warp][g][nt * 8 + 2 * t] = c[nt][0];
-    red[warp][g][nt * 8 + 2 * t + 1] = c[nt][1];
-    red[warp][g + 8][nt * 8 + 2 * t] = c[nt][2];
-    red[warp][g + 8][nt * 8 + 2 * t + 1] = c[nt][3];
+#pragma unroll
+    for (int q = 1; q < kAcc; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[nt][0][j] += c[nt][q][j];
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    red[warp][g][nt * 8 + 2 * t] = c[nt][0][0];
+    red[warp][g][nt * 8 + 2 * t + 1] = c[nt][0][1];
+    red[warp][g + 8][nt * 8 + 2 * t] = c[nt][0][2];
+    red[warp][g + 8][nt * 8 + 2 * t + 1] = c[nt][0][3];
   }
   __syncthreads();
   for (int o = threadIdx.x; o < kSkRows * BN; o += 32 * NW) {
