@@ -321,9 +321,9 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
         mbar_expect_tx(wbig, (uint32_t)((pre - s0) * 2048 * WB));
         w_run(s0, pre - s0, s0 / 2, wbig);
       }
-      // phase 0 of the slots' own barriers is not used by these chunks: complete it now, so that a
-      // slot's second use (chunk c + kWSlots) is its phase 1
-      for (int c = 0; c < n_pre; ++c) mbar_arrive(wfull(c));
+      // these chunks complete wbig0 / wbig, not the slots' own barriers: a slot's first wfull phase
+      // is its second use (chunk c + kWSlots; chunks beyond the prefetch exist only when
+      // n_pre == kWSlots), see the converters' parity
     } else {
       if (part & 2)
         for (int c = 0; c < n_pre; ++c) issue_w(c);
@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
     for (int j = par; j < nloc; j += 2) {
       const int c = j / L::kKpc, q = j % L::kKpc;  // kKpc == 2: each parity reads one step per chunk
       if (tiled && c < n_pre) mbar_wait(2 * c < pre_s0 ? wbig0 : wbig, 0);
-      else mbar_wait(wfull(c % L::kWSlots), (c / L::kWSlots) & 1);
+      else mbar_wait(wfull(c % L::kWSlots), ((c / L::kWSlots) - (tiled ? 1 : 0)) & 1);
       if (lane == 0 && (cw & 3) == 0) TRACE(3, j);
       if (lane == 0 && cw == 0 && j == 0) GTRACE(2);
       uint4 v[WB];
