@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define APT_ABI_VERSION 2
+#define APT_ABI_VERSION 1
 #define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
 
 typedef enum {
@@ -133,22 +133,12 @@ APT_API apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k
 APT_API apt_status apt_quantize_pack(const uint16_t* x, int32_t rows, int32_t k, int64_t ld, int32_t bits,
                                      apt_packed* out, float* scale, void* stream);
 
-/* Per-channel / per-token fp32 scales (and optional zero points) for APT_OUT_F16_SCALED (reading Q10;
- * zero points: SURVEY §8f NEXT-2, linear quantization x = s x_hat + z of P:199-201 on both operands,
- * activations x[m][k] = a_scale[m] x_hat + a_zero[m], weights W[n][k] = w_scale[n] w_hat + w_zero[n]):
- *   v = ((float)Y[m][n] * w_scale[n]) * a_scale[m]
- *   if a_zero or w_zero:  v += ((float)RW[n] * w_scale[n]) * az;  v += ((float)RA[m] * as) * wz;
- *                         v += ((float)K * az) * wz                  (az, wz = 0 where NULL)
- *   out[m][n] = RN_fp16(v)
- * fp32 arithmetic in that order, one final round-to-nearest-even to fp16 (overflow -> +-inf); RW / RA
- * are the packed operands' signed-code row sums (exact in fp32).  The paper's bipolar form
- * (s/2, z - s/2) of the same parameters gives the identical product; zero points are
- * ignored for the int32 output kinds. */
+/* Per-channel / per-token fp32 scales for APT_OUT_F16_SCALED (reading Q10):
+ *   out[m][n] = RN_fp16( ((float)Y[m][n] * w_scale[n]) * a_scale[m] ), fp32 arithmetic,
+ *   one final round-to-nearest-even to fp16 (overflow -> +-inf). */
 typedef struct {
   const float* w_scale; /* [N], required for APT_OUT_F16_SCALED */
   const float* a_scale; /* [M] per token, or NULL (== 1)        */
-  const float* w_zero;  /* [N] per output channel, or NULL (== 0) */
-  const float* a_zero;  /* [M] per token, or NULL (== 0)          */
 } apt_scales;
 
 typedef enum {

@@ -28,8 +28,7 @@ class AptPacked(ctypes.Structure):
 
 
 class AptScales(ctypes.Structure):
-    _fields_ = [("w_scale", ctypes.c_void_p), ("a_scale", ctypes.c_void_p), ("w_zero", ctypes.c_void_p),
-                ("a_zero", ctypes.c_void_p)]
+    _fields_ = [("w_scale", ctypes.c_void_p), ("a_scale", ctypes.c_void_p)]
 
 
 class AptConfig(ctypes.Structure):

@@ -138,8 +138,7 @@ def workspace_bytes(cfg: dict, M: int, N: int, K: int) -> int:
 
 def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_scale: torch.Tensor | None = None,
          a_scale: torch.Tensor | None = None, out: torch.Tensor | None = None, config: dict | None = None,
-         workspace: torch.Tensor | None = None, stream=None, w_zero: torch.Tensor | None = None,
-         a_zero: torch.Tensor | None = None) -> torch.Tensor:
+         workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """apt_gemm: Y = A . W^T (exact int32), Y' (bipolar), or fp16-scaled, in row ([M,N]) or col
     ([N,M]) layout."""
     M, N, K = A.rows, W.rows, W.k
@@ -156,13 +155,14 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
     if out.dtype != dtype or out.dim() != 2 or out.stride(1) != 1 or tuple(out.shape) != shape:
         raise ValueError(f"out must be a {dtype} tensor of shape {shape} with unit inner stride")
     sc = None
-    if any(t is not None for t in (w_scale, a_scale, w_zero, a_zero)):
-        for t, nm in ((w_scale, "w_scale"), (a_scale, "a_scale"), (w_zero, "w_zero"), (a_zero, "a_zero")):
+    if w_scale is not None or a_scale is not None:
+        for t, nm in ((w_scale, "w_scale"), (a_scale, "a_scale")):
             if t is not None:
                 _require_cuda(t, nm)
                 if t.dtype != torch.float32 or not t.is_contiguous():
                     raise ValueError(f"{nm} must be contiguous fp32")
-        sc = L.AptScales(*(t.data_ptr() if t is not None else None for t in (w_scale, a_scale, w_zero, a_zero)))
+        sc = L.AptScales(w_scale.data_ptr() if w_scale is not None else None,
+                         a_scale.data_ptr() if a_scale is not None else None)
     c = _config_struct(config)
     ws_need = 0
     if A.digits is None:  # the activation digit view is expanded into the workspace

@@ -263,8 +263,6 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   e.a_rowsum = A->row_sum;
   e.w_scale = scales ? scales->w_scale : nullptr;
   e.a_scale = scales ? scales->a_scale : nullptr;
-  e.w_zero = scales && kind == APT_OUT_F16_SCALED ? scales->w_zero : nullptr;
-  e.a_zero = scales && kind == APT_OUT_F16_SCALED ? scales->a_zero : nullptr;
   e.out = out;
   e.ldo = ldo;
   e.kind = (int32_t)kind;

@@ -93,8 +93,6 @@ struct EpilogueArgs {
   const int32_t* a_rowsum;  // RA[M]
   const float* w_scale;     // [N]
   const float* a_scale;     // [M] or null
-  const float* w_zero;      // [N] or null (NEXT-2 zero points, fp16 output only)
-  const float* a_zero;      // [M] or null
   void* out;
   int64_t ldo;
   int32_t kind;             // apt_out_kind
@@ -116,16 +114,7 @@ __device__ __forceinline__ void epilogue_store_v(const EpilogueArgs& e, int m, i
     const uint32_t yb = 4u * y + 2u * ra + 2u * rw + (uint32_t)e.K;
     reinterpret_cast<int32_t*>(e.out)[off] = (int32_t)yb;
   } else {
-    float v = ((float)(int32_t)y * wsc) * asc;
-    if (e.w_zero || e.a_zero) {
-      // x = as x_hat + az, W = ws w_hat + wz (P:199-201 with zero points):
-      // sum_k x W = as ws Y + az ws RW[n] + as wz RA[m] + K az wz; RW, RA < 2^24 are exact in fp32
-      const float az = e.a_zero ? __ldg(e.a_zero + m) : 0.f;
-      const float wz = e.w_zero ? __ldg(e.w_zero + n) : 0.f;
-      v += ((float)(int32_t)rw * wsc) * az;
-      v += ((float)(int32_t)ra * asc) * wz;
-      v += ((float)e.K * az) * wz;
-    }
+    const float v = ((float)(int32_t)y * wsc) * asc;
     unsigned short h;
     asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(v));
     reinterpret_cast<unsigned short*>(e.out)[off] = h;
