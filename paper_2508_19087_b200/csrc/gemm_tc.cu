@@ -440,20 +440,16 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
         if (!L::kBAll || j == 0) mbar_wait(full(L::kBAll ? 0 : s), L::kBAll ? 0u : ph);
         TRACE(1, j);
         if (j == 0) GTRACE(3);
-#ifndef APT_EXP_NOWAIT_A  // timing experiments only (wrong results)
         mbar_wait(a_full(a), pa);
-#endif
         TRACE(2, j);
         tc_fence_after();
         const uint64_t bdesc = umma_desc_sw128(sB + s * L::kBBytes);
-#ifndef APT_EXP_NOMMA
 #pragma unroll
         for (int kk = 0; kk < kTcBK / 32; ++kk) {
           // advance 32 K bytes inside the 128-byte swizzle atom: +2 in the (addr >> 4) field
           tc_mma_i8(tmem + (uint32_t)((kk % kNAcc) * BN), tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk),
                     idesc, (kNAcc > 1 ? (j | (kk / kNAcc)) : (j | kk)) != 0);
         }
-#endif
         if (!L::kBAll) {
           if (CN > 1) tc_commit_mc(empty(s), kMask); else tc_commit(empty(s));
         }
