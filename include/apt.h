@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define APT_ABI_VERSION 1
+#define APT_ABI_VERSION 2
 #define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
 
 typedef enum {
@@ -135,10 +135,20 @@ APT_API apt_status apt_quantize_pack(const uint16_t* x, int32_t rows, int32_t k,
 
 /* Per-channel / per-token fp32 scales for APT_OUT_F16_SCALED (reading Q10):
  *   out[m][n] = RN_fp16( ((float)Y[m][n] * w_scale[n]) * a_scale[m] ), fp32 arithmetic,
- *   one final round-to-nearest-even to fp16 (overflow -> +-inf). */
+ *   one final round-to-nearest-even to fp16 (overflow -> +-inf).
+ * Optional zero points (linear quantization x = s x_hat + z of P:199-201 on both
+ * operands: activations a_scale[m] x_hat + a_zero[m], weights w_scale[n] w_hat + w_zero[n]):
+ *   v = ((float)Y * w_scale[n]) * a_scale[m];  v += ((float)RW[n] * w_scale[n]) * az;
+ *   v += ((float)RA[m] * as) * wz;  v += ((float)K * az) * wz;  out = RN_fp16(v)
+ * (az, wz = 0 where NULL; RW / RA the packed row sums).  With zero points the GEMM writes the exact
+ * int32 Y into the workspace and a second elementwise pass applies the formula, so the workspace
+ * must hold apt_gemm_zp_workspace_bytes(); without them nothing changes.  Zero points are ignored
+ * for the int32 output kinds. */
 typedef struct {
   const float* w_scale; /* [N], required for APT_OUT_F16_SCALED */
   const float* a_scale; /* [M] per token, or NULL (== 1)        */
+  const float* w_zero;  /* [N] per output channel, or NULL (== 0) */
+  const float* a_zero;  /* [M] per token, or NULL (== 0)          */
 } apt_scales;
 
 typedef enum {
@@ -197,6 +207,10 @@ APT_API apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wb
 
 /* Host.  Device workspace bytes apt_gemm needs for (cfg, M, N, K).  0 = none. */
 APT_API size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K);
+
+/* Host.  Device workspace bytes apt_gemm needs for (cfg, M, N, K) when the scales carry zero points
+ * (fp16 output): the apt_gemm_workspace_bytes area rounded up to 16 bytes, then int32 Y [M][N]. */
+APT_API size_t apt_gemm_zp_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K);
 
 /* The W_p x A_q GEMM (§3.2 + §4.2): out = epilogue(A . W^T), exact in int32.
  *   W, A      : host structs describing device buffers produced by apt_pack_bipolar

@@ -17,7 +17,7 @@ APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
 APT_KERNEL_AUTO, APT_KERNEL_MMA_SPLITK, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY = 0, 1, 2, 3, 4
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
-EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes",
+EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes", "apt_gemm_zp_workspace_bytes",
             "apt_gemm", "apt_status_string", "apt_abi_version"]
 
 
@@ -28,7 +28,8 @@ class AptPacked(ctypes.Structure):
 
 
 class AptScales(ctypes.Structure):
-    _fields_ = [("w_scale", ctypes.c_void_p), ("a_scale", ctypes.c_void_p)]
+    _fields_ = [("w_scale", ctypes.c_void_p), ("a_scale", ctypes.c_void_p), ("w_zero", ctypes.c_void_p),
+                ("a_zero", ctypes.c_void_p)]
 
 
 class AptConfig(ctypes.Structure):
@@ -69,6 +70,9 @@ def lib():
         L.apt_gemm_workspace_bytes.restype = ctypes.c_size_t
         L.apt_gemm_workspace_bytes.argtypes = [ctypes.POINTER(AptConfig), ctypes.c_int32, ctypes.c_int32,
                                                ctypes.c_int32]
+        L.apt_gemm_zp_workspace_bytes.restype = ctypes.c_size_t
+        L.apt_gemm_zp_workspace_bytes.argtypes = [ctypes.POINTER(AptConfig), ctypes.c_int32, ctypes.c_int32,
+                                                  ctypes.c_int32]
         L.apt_gemm.restype = ctypes.c_int
         L.apt_gemm.argtypes = [ctypes.c_int32] * 5 + [ctypes.POINTER(AptPacked), ctypes.POINTER(AptPacked),
                                                       ctypes.POINTER(AptScales), ctypes.c_int, ctypes.c_int,

@@ -138,7 +138,8 @@ def workspace_bytes(cfg: dict, M: int, N: int, K: int) -> int:
 
 def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_scale: torch.Tensor | None = None,
          a_scale: torch.Tensor | None = None, out: torch.Tensor | None = None, config: dict | None = None,
-         workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+         workspace: torch.Tensor | None = None, stream=None, w_zero: torch.Tensor | None = None,
+         a_zero: torch.Tensor | None = None) -> torch.Tensor:
     """apt_gemm: Y = A . W^T (exact int32), Y' (bipolar), or fp16-scaled, in row ([M,N]) or col
     ([N,M]) layout."""
     M, N, K = A.rows, W.rows, W.k
@@ -155,22 +156,23 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
     if out.dtype != dtype or out.dim() != 2 or out.stride(1) != 1 or tuple(out.shape) != shape:
         raise ValueError(f"out must be a {dtype} tensor of shape {shape} with unit inner stride")
     sc = None
-    if w_scale is not None or a_scale is not None:
-        for t, nm in ((w_scale, "w_scale"), (a_scale, "a_scale")):
+    if any(t is not None for t in (w_scale, a_scale, w_zero, a_zero)):
+        for t, nm in ((w_scale, "w_scale"), (a_scale, "a_scale"), (w_zero, "w_zero"), (a_zero, "a_zero")):
             if t is not None:
                 _require_cuda(t, nm)
                 if t.dtype != torch.float32 or not t.is_contiguous():
                     raise ValueError(f"{nm} must be contiguous fp32")
-        sc = L.AptScales(w_scale.data_ptr() if w_scale is not None else None,
-                         a_scale.data_ptr() if a_scale is not None else None)
+        sc = L.AptScales(*(t.data_ptr() if t is not None else None for t in (w_scale, a_scale, w_zero, a_zero)))
     c = _config_struct(config)
     ws_need = 0
-    if A.digits is None:  # the activation digit view is expanded into the workspace
+    zp = kind == L.APT_OUT_F16_SCALED and (w_zero is not None or a_zero is not None)
+    if A.digits is None or zp:  # digit view expanded into the workspace / int32 Y for the zero points
         cc = c
         if cc is None:
             cc = L.AptConfig()
             L.check("apt_select_config", L.lib().apt_select_config(M, N, K, W.bits, A.bits, ctypes.byref(cc)))
-        ws_need = int(L.lib().apt_gemm_workspace_bytes(ctypes.byref(cc), M, N, K))
+        fn = L.lib().apt_gemm_zp_workspace_bytes if zp else L.lib().apt_gemm_workspace_bytes
+        ws_need = int(fn(ctypes.byref(cc), M, N, K))
     if ws_need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < ws_need):
         workspace = torch.empty((ws_need,), dtype=torch.uint8, device=W.planes.device)
     ws_ptr = workspace.data_ptr() if workspace is not None else None

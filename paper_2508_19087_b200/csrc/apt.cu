@@ -74,6 +74,10 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
   return APT_ERR_UNSUPPORTED;
 }
 
+// the product kernels behind apt_gemm (defined after the C ABI)
+apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_packed* A, const apt::EpilogueArgs& e,
+                          int32_t M, int32_t N, int32_t wbits, int32_t abits, void* workspace, cudaStream_t s);
+
 }  // namespace
 
 extern "C" {
@@ -229,6 +233,11 @@ size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int
   return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
 }
 
+size_t apt_gemm_zp_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
+  if (!cfg || M <= 0 || N <= 0 || K <= 0) return 0;
+  return (apt_gemm_workspace_bytes(cfg, M, N, K) + 15) / 16 * 16 + (size_t)M * (size_t)N * 4u;
+}
+
 apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, const apt_packed* W,
                     const apt_packed* A, const apt_scales* scales, apt_out_kind kind, apt_layout layout,
                     void* out, int64_t ldo, const apt_config* cfg, void* workspace, size_t ws_bytes,
@@ -254,7 +263,12 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   }
   st = validate_config(&c, M, N, K, wbits, abits);
   if (st != APT_OK) return st;
-  const size_t need = (A->digits && c.kernel != APT_KERNEL_MMA_SPLITK) ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
+  const size_t need0 = (A->digits && c.kernel != APT_KERNEL_MMA_SPLITK) ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
+  // zero points (NEXT-2): exact int32 Y into the workspace after the digit-expansion area, then the
+  // elementwise zero-point epilogue
+  const bool zp = kind == APT_OUT_F16_SCALED && (scales->w_zero || scales->a_zero);
+  const size_t y_off = (need0 + 15) / 16 * 16;
+  const size_t need = zp ? y_off + (size_t)M * (size_t)N * 4u : need0;
   if (need > 0 && (!workspace || ws_bytes < need || !aligned16(workspace))) return APT_ERR_WORKSPACE;
   if (A->digits && !aligned16(A->digits)) return APT_ERR_INVALID_ARGUMENT;
 
@@ -274,6 +288,36 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   e.h_w = 1 << (wbits - 1);
   e.h_a = 1 << (abits - 1);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (zp) {
+    e.out = reinterpret_cast<uint8_t*>(workspace) + y_off;
+    e.ldo = N;
+    e.kind = APT_OUT_I32_SIGNED;
+    e.layout = APT_LAYOUT_ROW;
+  }
+  st = launch_product(c, W, A, e, M, N, wbits, abits, workspace, s);
+  if (st != APT_OK || !zp) return st;
+  apt::ZpArgs z;
+  z.y = reinterpret_cast<const int32_t*>(reinterpret_cast<uint8_t*>(workspace) + y_off);
+  z.w_rowsum = W->row_sum;
+  z.a_rowsum = A->row_sum;
+  z.w_scale = scales->w_scale;
+  z.a_scale = scales->a_scale;
+  z.w_zero = scales->w_zero;
+  z.a_zero = scales->a_zero;
+  z.out = reinterpret_cast<__half*>(out);
+  z.ldo = ldo;
+  z.layout = (int32_t)layout;
+  z.M = M;
+  z.N = N;
+  z.K = K;
+  return apt::launch_zp_epilogue(z, s) == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+}
+
+}  // extern "C"
+
+namespace {
+apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_packed* A, const apt::EpilogueArgs& e,
+                          int32_t M, int32_t N, int32_t wbits, int32_t abits, void* workspace, cudaStream_t s) {
   if (c.kernel == APT_KERNEL_MMA_SPLITK) {
     if (W->layout != APT_PACK_ROWS || A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
     apt::MmaArgs p;
@@ -322,5 +366,4 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   }
   return APT_ERR_UNSUPPORTED;
 }
-
-}  // extern "C"
+}  // namespace

@@ -1,6 +1,7 @@
 // kernels.h — launch interfaces between the C-ABI shim (apt.cu) and the kernels.
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -67,4 +68,18 @@ struct GemvArgs {
 cudaError_t launch_gemv(const GemvArgs& p, int wbits, int warps, cudaStream_t stream);  // warps: 8 or 16
 // M <= 16: mma.sync m16n8k32 u8 skinny GEMM fed from registers (gemm_skinny.cu); bn 8 or 16, warps 4/8/16
 cudaError_t launch_gemm_skinny(const GemvArgs& p, int wbits, int bn, int warps, cudaStream_t stream);
+}  // namespace apt
+
+namespace apt {
+// fp16 output with zero points from the exact int32 Y (epilogue_zp.cu)
+struct ZpArgs {
+  const int32_t* y;         // [M][N] row-major, signed product
+  const int32_t* w_rowsum;  // RW[N]
+  const int32_t* a_rowsum;  // RA[M]
+  const float *w_scale, *a_scale, *w_zero, *a_zero;
+  __half* out;
+  int64_t ldo;
+  int32_t layout, M, N, K;
+};
+cudaError_t launch_zp_epilogue(const ZpArgs& p, cudaStream_t stream);
 }  // namespace apt

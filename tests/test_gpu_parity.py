@@ -477,3 +477,36 @@ def test_skinny_llama7b_full(n, k, m, pw, pa):
     A, W = _pack_both(a, pa, w, pw)
     got = P.gemm(W, A, config=_skinny_cfg(m, n, k, pw, pa, bn=8 if m <= 8 else 16)).cpu().numpy().astype(np.int64)
     assert np.array_equal(got, c_gemm_i64(a, w))
+
+
+# ----------------------------------------------------------------------------- zero-point epilogue (NEXT-2)
+
+@pytest.mark.parametrize("m,n,k", [(1, 300, 1000), (5, 300, 1000), (16, 200, 4096), (300, 256, 1000)])
+@pytest.mark.parametrize("zeros", ["a", "w", "both"])
+def test_zero_point_epilogue(m, n, k, zeros):
+    """fp16 output with zero points (apt_scales.w_zero / a_zero: int32 Y of every kernel family the
+    selector reaches — GEMV, skinny, tcgen05 decode and prefill tiles — then the zero-point pass) vs
+    the fp64 dequantize-then-multiply
+    oracle.  Bound: fp32 evaluation of four terms + one fp16 rounding, relative to the sum of the
+    terms' magnitudes (cancellation-safe): 1e-3 * (|t1| + |t2| + |t3| + |t4|) + 2^-24."""
+    pa, pw = 4, 3
+    a = signed_codes(m, k, pa, seed=90 + m)
+    w = signed_codes(n, k, pw, seed=91 + n)
+    rng = np.random.default_rng(m + n)
+    ws = log_uniform_scales(n, -10, -6, seed=7)
+    as_ = log_uniform_scales(m, -6, -2, seed=8)
+    wz = (rng.uniform(-1, 1, n) * 2.0 ** -8).astype(np.float32) if zeros in ("w", "both") else None
+    az = rng.uniform(-1, 1, m).astype(np.float32) * 2.0 ** -3 if zeros in ("a", "both") else None
+    az = az.astype(np.float32) if az is not None else None
+    A, W = _pack_both(a, pa, w, pw)
+    got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_),
+                 w_zero=_dev(wz) if wz is not None else None, a_zero=_dev(az) if az is not None else None)
+    got = got.cpu().numpy().astype(np.float64)
+    ref = O.dequant_gemm_fp64(a, w, ws, as_, wz, az)
+    y = O.gemm_signed(a, w).astype(np.float64)
+    ra, rw = a.astype(np.float64).sum(1), w.astype(np.float64).sum(1)
+    az0 = np.zeros(m) if az is None else az.astype(np.float64)
+    wz0 = np.zeros(n) if wz is None else wz.astype(np.float64)
+    mag = (np.abs(y * ws[None, :] * as_[:, None]) + np.abs(rw[None, :] * ws[None, :] * az0[:, None]) +
+           np.abs(ra[:, None] * as_[:, None] * wz0[None, :]) + np.abs(k * az0[:, None] * wz0[None, :]))
+    assert (np.abs(got - ref) <= 1e-3 * mag + 2.0 ** -24).all()
