@@ -65,13 +65,15 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+KERNEL_NAMES = {1: "gemm_mma_kernel (mma.sync)", 2: "gemm_tc_kernel (tcgen05)", 3: "gemv_kernel (SIMT dp4a)",
+                4: "gemm_skinny_kernel (mma.sync from registers)"}
+
+
 def kernel_mix(cfgs):
     """Launch count per kernel family of one GEMM phase (from the selector's configs)."""
-    names = {1: "gemm_mma_kernel (mma.sync)", 2: "gemm_tc_kernel (tcgen05)", 3: "gemv_kernel (SIMT dp4a)",
-             4: "gemm_skinny_kernel (mma.sync from registers)"}
     mix = {}
     for c in cfgs:
-        mix[names[c["kernel"]]] = mix.get(names[c["kernel"]], 0) + 1
+        mix[KERNEL_NAMES[c["kernel"]]] = mix.get(KERNEL_NAMES[c["kernel"]], 0) + 1
     return mix
 
 
@@ -346,7 +348,7 @@ def main():
     hbm_peak, peak_src = load_peaks()
     achieved = bytes_all / (gemm_ms * 1e-3) / 1e9
     traffic = load_traffic()
-    per_prec, per_m = breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, shard, layout,
+    per_prec, per_m, per_kernel = breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, shard, layout,
                                 use_graphs, hbm_peak)
     line = {"metric": METRIC, "value": round(value, 4), "unit": "TOPS",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
@@ -370,7 +372,7 @@ def main():
                          "gemm_share_of_step": round(gemm_ms / ms_per_step, 3),
                          "gemm_us_per_launch": round(1e3 * gemm_ms / len(CASES), 3)},
             "act_pack": {"launches_per_step": len(A_codes), "us_per_step": round(1e3 * pack_ms, 3)},
-            "per_precision": per_prec, "per_m": per_m,
+            "per_precision": per_prec, "per_m": per_m, "per_kernel": per_kernel,
             "weight_pack": {"ms": round(wpack_ms, 3), "GB/s": round(wpack_bytes / (wpack_ms * 1e-3) / 1e9, 1)}}
 
     log("baselines")
@@ -427,8 +429,12 @@ def breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, s
     per_prec = {f"W{wb}A{ab}": group_stats([i for i, c in enumerate(CASES) if c[1] == wb and c[2] == ab])
                 for (wb, ab) in PRECISIONS}
     per_m = {f"M{m}": group_stats([i for i, c in enumerate(CASES) if c[0] == m]) for m in MS}
+    # per kernel family (the selector's choice per case): each family's own HBM roofline fraction
+    fams = sorted({c["kernel"] for c in cfgs})
+    per_kernel = {KERNEL_NAMES[f]: dict(group_stats([i for i, c in enumerate(cfgs) if c["kernel"] == f]),
+                                        launches=sum(1 for c in cfgs if c["kernel"] == f)) for f in fams}
     del flush
-    return per_prec, per_m
+    return per_prec, per_m, per_kernel
 
 
 def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout, value, barrier):
