@@ -20,9 +20,22 @@
  *   - All calls taking a stream are stream-ordered and asynchronous; the library never
  *     synchronizes, never allocates device memory, and keeps no per-call state.
  *     Argument errors are returned synchronously before anything is launched.
+ *   - Stream order and programmatic dependent launch (PDL): every kernel is launched with
+ *     programmatic stream serialization.  apt_gemm's kernels read the WEIGHT-side operands
+ *     (W planes, W row sums, w_scale) before waiting for their stream predecessor, so that the next
+ *     GEMM's weights stream from HBM while the previous kernel finishes; activation-side operands
+ *     and the output are touched only after the wait.  This is safe whenever the kernel that wrote the
+ *     weight-side buffers did not release its dependents early: apt_pack_bipolar / apt_quantize_pack
+ *     never do (their dependents start after every CTA has exited, stores fenced at GPU scope), and
+ *     ordinary kernels (torch, cuBLAS, memcpy) never do.  Only a caller kernel that itself executes
+ *     griddepcontrol.launch_dependents / cudaTriggerProgrammaticLaunchCompletion BEFORE writing the
+ *     weights of the apt_gemm that follows it on the same stream breaks this; insert an event or
+ *     any non-PDL kernel between them.
  *   - The caller owns every buffer (in practice torch tensors).
  *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
- *   - Thread-safe: the only global state is a mutex-guarded cache of device attributes.
+ *   - Thread-safe: the only global state is the per-device SM count (queried once under a mutex), the
+ *     driver entry point of cuTensorMapEncodeTiled (resolved once) and per-kernel "max dynamic shared
+ *     memory set" flags (atomics).  Tensor maps are encoded per call on the host (no cache).
  *   - There is no CPU fallback: with no CUDA device every launching call returns APT_ERR_CUDA.
  */
 #ifndef APT_H_
@@ -41,7 +54,7 @@
 extern "C" {
 #endif
 
-#define APT_ABI_VERSION 2
+#define APT_ABI_VERSION 3
 #define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
 
 typedef enum {
@@ -78,6 +91,9 @@ typedef enum {
  *             two's-complement code).  Element c of a row is bit (c % 32) of word (c / 32),
  *             LSB first (reading Q5).  Pad elements c in [k, Kpad) hold the signed code 0,
  *             i.e. u = 2^(n-1) (reading Q6), so they contribute exactly 0 to signed products.
+ *             NOTE: this differs from the SPEC's zero-bit padding (pads = bipolar -1): planes
+ *             padded with zero bits are NOT valid input to apt_gemm (the epilogue assumes signed-0
+ *             pads); produce packed operands with apt_pack_bipolar / apt_quantize_pack only.
  *             Must be 16-byte aligned.
  *   row_sum : int32 [rows], sum_{c<k} of the signed codes of the row (used by the rank-1 terms of
  *             the epilogue; SURVEY §8c identities I2/I3).
@@ -164,8 +180,7 @@ typedef enum {
 
 typedef enum {
   APT_KERNEL_AUTO = 0,
-  APT_KERNEL_MMA_SPLITK = 1, /* register-rebuild mma.sync u8 kernel, split-K reduced in a thread-block
-                                cluster through distributed shared memory (decode / small M)     */
+  /* 1 was APT_KERNEL_MMA_SPLITK (ABI <= 2, removed: never selected, superseded by APT_KERNEL_SKINNY) */
   APT_KERNEL_TC = 2,         /* tcgen05 kind::i8 kernel: weights rebuilt in registers -> TMEM (A operand),
                                 tokens via TMA from the int8 token workspace, s32 accumulator in TMEM */
   APT_KERNEL_GEMV = 3,       /* M <= 4: SIMT GEMV, weights rebuilt in registers (same u8 digits), dp4a
@@ -185,12 +200,17 @@ typedef enum {
  *   bn       : tokens per CTA tile (MMA N side)
  *   bk       : K elements per pipeline step
  *   stages   : pipeline depth (TC kernel)
- *   split_k  : K splits (MMA_SPLITK / TC kernels: the cluster size, 1..8; GEMV: warps per CTA, 8 or 16)
+ *   split_k  : K splits (TC kernel: CTAs of a (1,1,S) cluster, 1..8; GEMV / SKINNY: warps per CTA)
  *   cta_pair : 1 = cta_group::2 pairs (TC kernel), 0 = single CTA (this build: 0)
  *   cluster_n: TC kernel: CTAs along N (weight tiles) sharing one token tile; the token tile is loaded
- *              once per cluster with TMA multicast (1, 2 or 4)                                          */
+ *              once per cluster with TMA multicast (1, 2 or 4)
+ *   mma_kind : tensor-core operand kind (apt_mma_kind)                                                  */
+typedef enum {
+  APT_MMA_I8 = 0    /* u8 x u8 -> s32 digits (tcgen05 kind::i8 / mma.sync u8 / dp4a)                  */
+} apt_mma_kind;
+
 typedef struct {
-  int32_t kernel, w_digit, a_digit, bm, bn, bk, stages, split_k, cta_pair, cluster_n;
+  int32_t kernel, w_digit, a_digit, bm, bn, bk, stages, split_k, cta_pair, cluster_n, mma_kind;
 } apt_config;
 
 /* Host, pure and deterministic (replaces the paper's lookup table + search, §5.2).

@@ -14,7 +14,9 @@ APT_OK, APT_ERR_INVALID_ARGUMENT, APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ER
 APT_ENC_SIGNED, APT_ENC_BIPOLAR = 0, 1
 APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
 APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
-APT_KERNEL_AUTO, APT_KERNEL_MMA_SPLITK, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY = 0, 1, 2, 3, 4
+APT_KERNEL_AUTO, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY = 0, 2, 3, 4
+APT_MMA_I8 = 0
+ABI_VERSION = 3  # include/apt.h APT_ABI_VERSION this binding marshals for
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes", "apt_gemm_zp_workspace_bytes",
@@ -35,7 +37,7 @@ class AptScales(ctypes.Structure):
 class AptConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
                 ("kernel", "w_digit", "a_digit", "bm", "bn", "bk", "stages", "split_k", "cta_pair",
-                 "cluster_n")]
+                 "cluster_n", "mma_kind")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -82,6 +84,9 @@ def lib():
         L.apt_status_string.argtypes = [ctypes.c_int]
         L.apt_abi_version.restype = ctypes.c_int32
         L.apt_abi_version.argtypes = []
+        v = int(L.apt_abi_version())
+        if v != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI version {v}, this binding needs {ABI_VERSION}: rebuild it")
         _lib = L
     return _lib
 

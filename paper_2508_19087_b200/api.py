@@ -76,6 +76,28 @@ def alloc_packed(rows: int, k: int, bits: int, device, digits: bool = False, til
     return Packed(planes, row_sum, rows, k, bits, dig, tiled)
 
 
+def _check_out(out: "Packed", rows: int, k: int, bits: int, tiled: bool, digits: bool):
+    """A caller-supplied output must describe exactly the buffers apt_pack_bipolar will write."""
+    want = alloc_shapes(rows, k, bits, digits, tiled)
+    if (out.rows, out.k, out.bits, bool(out.tiled)) != (rows, k, bits, bool(tiled)):
+        raise ValueError(f"out describes (rows={out.rows}, k={out.k}, bits={out.bits}, tiled={out.tiled}), "
+                         f"the codes need (rows={rows}, k={k}, bits={bits}, tiled={tiled})")
+    for name, t, shape, dt in (("planes", out.planes, want[0], torch.int32), ("row_sum", out.row_sum, want[1], torch.int32),
+                               ("digits", out.digits, want[2], torch.uint8)):
+        if shape is None:
+            continue
+        if t is None or tuple(t.shape) != shape or t.dtype != dt or not t.is_contiguous():
+            raise ValueError(f"out.{name} must be a contiguous {dt} tensor of shape {shape}")
+    if out.planes.device != out.row_sum.device:
+        raise ValueError("out buffers live on different devices")
+
+
+def alloc_shapes(rows: int, k: int, bits: int, digits: bool, tiled: bool):
+    kw = kpad(k) // 32
+    prow = -(-rows // 128) * 128 if tiled else rows
+    return (bits, prow, kw), (rows,), ((rows, kw * 32) if digits else None)
+
+
 def pack(codes: torch.Tensor, bits: int, encoding: str = "signed", out: Packed | None = None,
          range_error: torch.Tensor | None = None, stream=None, digits: bool = False, tiled: bool = False) -> Packed:
     """apt_pack_bipolar: int8 codes [rows, k] (row stride ``codes.stride(0)``) -> Packed.
@@ -87,6 +109,10 @@ def pack(codes: torch.Tensor, bits: int, encoding: str = "signed", out: Packed |
     rows, k = codes.shape
     if out is None:
         out = alloc_packed(rows, k, bits, codes.device, digits=digits, tiled=tiled)
+    else:
+        _check_out(out, rows, k, bits, out.tiled, out.digits is not None)
+        if out.planes.device != codes.device:
+            raise ValueError("out lives on another device than codes")
     st = out.struct()
     rc = L.lib().apt_pack_bipolar(codes.data_ptr(), rows, k, codes.stride(0), bits, _ENCODINGS[encoding],
                                   ctypes.byref(st), range_error.data_ptr() if range_error is not None else None,
@@ -106,8 +132,14 @@ def quantize_pack(x: torch.Tensor, bits: int, out: Packed | None = None, scale: 
     rows, k = x.shape
     if out is None:
         out = alloc_packed(rows, k, bits, x.device, digits=digits, tiled=tiled)
+    else:
+        _check_out(out, rows, k, bits, out.tiled, out.digits is not None)
+        if out.planes.device != x.device:
+            raise ValueError("out lives on another device than x")
     if scale is None:
         scale = torch.empty(rows, dtype=torch.float32, device=x.device)
+    elif scale.dtype != torch.float32 or not scale.is_contiguous() or scale.numel() < rows or scale.device != x.device:
+        raise ValueError("scale must be a contiguous fp32 tensor of >= rows elements on x's device")
     st = out.struct()
     rc = L.lib().apt_quantize_pack(x.data_ptr(), rows, k, x.stride(0), bits, ctypes.byref(st), scale.data_ptr(),
                                    _stream_handle(stream))

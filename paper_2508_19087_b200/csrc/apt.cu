@@ -2,6 +2,7 @@
 // kernel dispatch.  No torch types, no allocation, no synchronization.
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/apt.h"
@@ -10,7 +11,29 @@
 
 namespace {
 
-constexpr int kNumSMs = 148;
+// The library's only global state (include/apt.h "Thread-safe"): the SM count of each device, queried
+// once under a mutex.  Without a device (CPU-only hosts) the B200's 148 is assumed, so the selector
+// stays a pure function of (M, N, K, p, q) on a given device.
+std::mutex g_dev_mu;
+int g_dev_sms[64] = {0};
+
+int device_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return 148;
+  }
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (g_dev_sms[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
+      v = 148;
+    }
+    g_dev_sms[dev] = v;
+  }
+  return g_dev_sms[dev];
+}
 
 
 int64_t kpad_of(int64_t k) { return ((k + APT_KPAD_QUANTUM - 1) / APT_KPAD_QUANTUM) * APT_KPAD_QUANTUM; }
@@ -36,15 +59,7 @@ apt_status validate_packed(const apt_packed* P, int32_t rows, int32_t k, int32_t
 apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits) {
   const int kw = (int)(kpad_of(K) / 32);
   if (c->w_digit != wbits || c->a_digit != abits) return APT_ERR_UNSUPPORTED;  // full-width digits only
-  (void)kw;
-  if (c->kernel == APT_KERNEL_MMA_SPLITK) {
-    if (c->bm != 32 || c->bk != 256) return APT_ERR_UNSUPPORTED;
-    if (c->bn != 8 && c->bn != 16) return APT_ERR_UNSUPPORTED;
-    if (c->split_k != 4) return APT_ERR_UNSUPPORTED;
-    if (apt::mma_depth(wbits, abits, c->bn, kw) < 2) return APT_ERR_UNSUPPORTED;
-    if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
-    return APT_OK;
-  }
+  if (c->mma_kind != APT_MMA_I8) return APT_ERR_UNSUPPORTED;
   if (c->kernel == APT_KERNEL_GEMV) {
     if (M > 4 || c->bm != 32 || c->bn != M || c->bk != 128 || (c->split_k != 8 && c->split_k != 16) ||
         c->stages != 1)
@@ -165,10 +180,10 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
     return APT_ERR_INVALID_ARGUMENT;
   if (!bound_ok(K, wbits, abits)) return APT_ERR_UNSUPPORTED;
   std::memset(out, 0, sizeof(*out));
+  const int kNumSMs = device_sms();
   const int kw = (int)(kpad_of(K) / 32);
   out->w_digit = wbits;
   out->a_digit = abits;
-  // every shape runs on the tcgen05 kernel (the mma.sync decode kernel stays selectable by config)
   out->kernel = APT_KERNEL_TC;
   out->bm = 128;
   out->bk = 128;
@@ -229,7 +244,7 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
 size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
   // TC kernel: activation digit view for activations packed without one (apt_packed.digits == NULL)
   (void)N;
-  if (!cfg || M <= 0 || K <= 0 || cfg->kernel == APT_KERNEL_MMA_SPLITK) return 0;
+  if (!cfg || M <= 0 || K <= 0) return 0;
   return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
 }
 
@@ -263,7 +278,7 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   }
   st = validate_config(&c, M, N, K, wbits, abits);
   if (st != APT_OK) return st;
-  const size_t need0 = (A->digits && c.kernel != APT_KERNEL_MMA_SPLITK) ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
+  const size_t need0 = A->digits ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
   // zero points (NEXT-2): exact int32 Y into the workspace after the digit-expansion area, then the
   // elementwise zero-point epilogue
   const bool zp = kind == APT_OUT_F16_SCALED && (scales->w_zero || scales->a_zero);
@@ -318,19 +333,6 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
 namespace {
 apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_packed* A, const apt::EpilogueArgs& e,
                           int32_t M, int32_t N, int32_t wbits, int32_t abits, void* workspace, cudaStream_t s) {
-  if (c.kernel == APT_KERNEL_MMA_SPLITK) {
-    if (W->layout != APT_PACK_ROWS || A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
-    apt::MmaArgs p;
-    p.wp = W->planes;
-    p.w_pstride = (int64_t)N * W->k_words;
-    p.ap = A->planes;
-    p.a_pstride = (int64_t)M * A->k_words;
-    p.k_words = W->k_words;
-    p.abits = abits;
-    p.e = e;
-    cudaError_t err = apt::launch_gemm_mma(p, wbits, c.bn, s);
-    return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
-  }
   // the TC kernel reads the activation operand as kernel-order u8 digits: the packed view, or
   // expanded now into the workspace
   const uint8_t* adig = A->digits;

@@ -16,7 +16,7 @@
 //     kernel) turns a word into 8 digit registers; register 2s / 2s+1 of word 2t+grp are the A
 //     fragment's k-slots [4t, 4t+4) / [16+4t, 16+4t+4) of K-step s of group grp, and the token
 //     operand takes the same registers of the same word from the activation digit view, so both
-//     operands agree on K (the mapping of gemm_mma.cu);
+//     operands agree on K;
 //   * 8 mma.sync per iteration and 8-token tile accumulate u8 x u8 into s32 (the add half);
 //   * epilogue: the warps' partial tiles are summed in shared memory and every output goes through
 //     epilogue_store_v (rank-1 correction, fp16 scale, row or column layout).

@@ -1,27 +1,31 @@
-// gemm_tc.cu — APT W_p x A_q GEMM on the 5th-generation tensor cores (tcgen05, kind::i8) for
-// prefill-sized token counts.
+// gemm_tc.cu — APT W_p x A_q GEMM on the 5th-generation tensor cores (tcgen05, kind::i8).
 //
 //   D[128 weight rows x BN tokens] (s32, TMEM) += A[128 x K] (u8 digits, TMEM) . B[BN x K]^T (u8, SMEM)
 //
-// Per CTA (8 warps, one 128 x BN output tile, 2 CTAs per SM at BN = 128):
-//   warp 0      TMA producer: per 128-element K step, one 3-D TMA box of ALL weight planes
-//               ({4 words, 128 rows, wbits planes}: the paper's concatenated "unified matrix", §4.1
-//               Step 3, moved with a single command) + one 2-D box of token digits
-//               (128 B x BN rows, 128-byte swizzle) into a `stages`-deep shared-memory ring.
+// Per CTA: 384 threads = 12 warps, one 128 x BN output tile (BN = 16 / 64 / 128 / 256):
+//   warp 0      producer (one thread): the weight planes of the CTA's K range — tile-major planes
+//               (APT_PACK_TILED) with cp.async.bulk runs, canonical planes with one 3-D TMA box per
+//               chunk ({words, 128 rows, wbits planes}: the paper's concatenated "unified matrix",
+//               §4.1 Step 3, moved with one command) — into a ring of weight slots, the first
+//               ring's worth before griddepcontrol.wait; then the token digits (2-D 128B-swizzled TMA
+//               boxes of the activation digit view): the whole K range at once for BN = 16, a
+//               `stages`-deep ring otherwise.
 //   warp 1      MMA issuer (one thread): 4 x tcgen05.mma.cta_group::1.kind::i8 (M=128, N=BN, K=32)
-//               per K step, A from TMEM, B from a shared-memory descriptor; tcgen05.commit frees
-//               the ring slots.
-//   warp 2      TMEM allocator.
-//   warps 4..7  converters, then epilogue.  Thread = weight row (= TMEM lane).  Per K step each
-//               thread reads its row's wbits x 16 B of planes, rebuilds the 128 u8 digits with
-//               rebuild8() (the shift half of the shift-add recovery) and writes them to the
-//               TMEM A ring with tcgen05.st — the planes never leave the SM in any other form
-//               (recovery-oriented scheduling, §4.2).  After the last MMA they load the
-//               accumulator with tcgen05.ld and apply the rank-1 correction + scale (common.cuh).
+//               per 128-element K step, A from the TMEM ring, B from a shared-memory descriptor;
+//               tcgen05.commit frees the ring slots and finally signals the accumulator.
+//   warps 2-3   TMEM allocation; epilogue operands (weight row sums / scales before the wait, token
+//               row sums / scales after).
+//   warps 4-11  converters (two per TMEM sub-partition, alternating K steps), then the epilogue.
+//               Thread = weight row (= TMEM lane).  Per K step each thread reads its row's wbits x 16 B
+//               of planes, rebuilds the 128 u8 digits with rebuild8() (the shift half of the shift-add
+//               recovery) and writes them to the TMEM A ring with tcgen05.st — the planes never
+//               leave the SM in any other form (recovery-oriented scheduling, §4.2).  After
+//               the last MMA they load the accumulator (tcgen05.ld) and apply the rank-1 correction +
+//               scale (common.cuh), or push split-K partials to the owning cluster rank over DSMEM.
 //
-// Token digits come from the per-call expand pre-pass (expand_tokens_kernel) which writes the
-// activation planes as u8 digits [M][Kpad] in the same within-word K order rebuild8() uses, so
-// both operands agree on K.
+// Token digits come from the activation digit view written by the pack kernel (apt_packed.digits),
+// or from expand_tokens_kernel into the workspace, in the same within-word K order rebuild8() uses,
+// so both operands agree on K.
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -654,14 +658,16 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
 
 // ------------------------------------------------------------------------------------ host side
 PFN_encodeTiled_t tensor_map_encoder() {
-  static PFN_encodeTiled_t fn = nullptr;
-  if (!fn) {
+  // resolved once (thread-safe static initialization)
+  static const PFN_encodeTiled_t fn = []() -> PFN_encodeTiled_t {
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled_t>(ptr);
-  }
+      return reinterpret_cast<PFN_encodeTiled_t>(ptr);
+    cudaGetLastError();
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -701,7 +707,7 @@ static cudaError_t launch_tc4(const CUtensorMap& tw, const CUtensorMap& tb, cons
   // the decode tiles are sized for two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
   static_assert(BN != 16 || 2 * (L::kTotal + 1024) <= 228 * 1024, "two CTAs per SM");
   auto kern = gemm_tc_kernel<WB, BN, ST, CN>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+  cudaError_t err = set_smem_once<gemm_tc_kernel<WB, BN, ST, CN>>(L::kTotal);
   if (err != cudaSuccess) return err;
   const int gx = ((p.e.N + kTcBM - 1) / kTcBM + CN - 1) / CN * CN;
   return launch_pdl(kern, dim3(gx, (p.e.M + BN - 1) / BN, split), dim3(384), L::kTotal, stream, dim3(CN, 1, split),

@@ -23,18 +23,6 @@ cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream);
 // fused fp16 -> per-row symmetric quantize -> pack (x: const __half*, scale: [rows] fp32 out)
 cudaError_t launch_quant_pack(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream);
 
-struct MmaArgs {
-  const uint32_t* wp;      // weight planes [wbits][N][k_words]
-  int64_t w_pstride;       // N * k_words
-  const uint32_t* ap;      // activation planes [abits][M][k_words]
-  int64_t a_pstride;       // M * k_words
-  int32_t k_words;
-  int32_t abits;
-  int32_t depth;           // per-warp TMA ring depth (set by launch_gemm_mma)
-  EpilogueArgs e;
-};
-cudaError_t launch_gemm_mma(const MmaArgs& p, int wbits, int bn, cudaStream_t stream);
-int mma_depth(int wbits, int abits, int bn, int k_words);  // 0 if the kernel does not fit
 // activation planes [abits][M][k_words] -> kernel-order u8 digits [M][Kpad]
 cudaError_t launch_expand_tokens(const uint32_t* ap, int64_t a_pstride, int M, int k_words, int abits,
                                  uint8_t* out, cudaStream_t stream);

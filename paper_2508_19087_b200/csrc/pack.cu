@@ -90,10 +90,16 @@ __device__ __forceinline__ void row_sum_store(const PackArgs& p, int r, int sum)
   }
 }
 
+// Stream order with programmatic dependent launch (include/apt.h "General contract"): the GEMMs
+// read weight-side operands (planes, row sums, scales) BEFORE griddepcontrol.wait, so a kernel that
+// writes them must not release its dependents early.  The pack kernels therefore never execute
+// griddepcontrol.launch_dependents (the dependents launch only once every CTA has exited) and make
+// their stores visible at GPU scope before exiting (pack_release).
+__device__ __forceinline__ void pack_release() { __threadfence(); }
+
 template <int BITS>
 __global__ void __launch_bounds__(1024) pack_kernel(PackArgs p) {
-  pdl_launch_dependents();  // the next kernel (a GEMM) may start streaming its weights now
-  pdl_wait();               // our codes / output buffers may still be in use by the previous kernel
+  pdl_wait();  // our codes / output buffers may still be in use by the previous kernel
   const int r = blockIdx.x;
   const int8_t* row = p.codes + (int64_t)r * p.ld;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0);
@@ -161,6 +167,7 @@ __global__ void __launch_bounds__(1024) pack_kernel(PackArgs p) {
     store_word<BITS>(p, r, w, u);
   }
   row_sum_store(p, r, sum);
+  pack_release();
 }
 
 cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream) {
@@ -192,8 +199,7 @@ cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream) {
 // the same precision as the oracle's.
 template <int BITS>
 __global__ void __launch_bounds__(1024) quant_pack_kernel(PackArgs p, const __half* __restrict__ x, float* scale) {
-  pdl_launch_dependents();
-  pdl_wait();
+  pdl_wait();  // no early trigger: see pack_release()
   const int r = blockIdx.x;
   const __half* row = x + (int64_t)r * p.ld;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0);
@@ -254,6 +260,7 @@ __global__ void __launch_bounds__(1024) quant_pack_kernel(PackArgs p, const __ha
     store_word<BITS>(p, r, w, u);
   }
   row_sum_store(p, r, sum);
+  pack_release();
 }
 
 cudaError_t launch_quant_pack(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {

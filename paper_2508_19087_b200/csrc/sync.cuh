@@ -1,5 +1,6 @@
 // sync.cuh — mbarrier / TMA PTX wrappers and the host tensor-map encoder (product path).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -63,9 +64,11 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                : "memory");
 }
 // Programmatic dependent launch: every kernel of the library is launched with programmatic stream
-// serialization, lets its successor launch immediately, and waits for its predecessor only right
-// before touching memory the predecessor may write (weights, row sums and scales of the weight side
-// are read before the wait: they are immutable across calls)
+// serialization.  The GEMMs let their successor launch immediately and wait for their predecessor only
+// right before touching memory a predecessor may write; weight-side operands (planes, row sums,
+// w_scale) are read before the wait.  That is safe because no kernel of this library that writes
+// them releases its dependents early (the pack kernels never trigger; see pack.cu pack_release), and
+// kernels of other libraries never trigger early either (include/apt.h "General contract").
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -93,6 +96,19 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = attr;
   cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel instantiation and device
+template <auto Kern>
+inline cudaError_t set_smem_once(int bytes) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorNoDevice;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

@@ -25,7 +25,7 @@ def test_header_symbols_exported():
     lib = L.lib()
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.apt_abi_version() == 2
+    assert lib.apt_abi_version() == L.ABI_VERSION == 3
 
 
 def test_status_strings():
@@ -62,10 +62,8 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab):
     assert c.as_dict() == c2.as_dict()
     kw = -(-K // 256) * 8
     assert c.w_digit == wb and c.a_digit == ab
-    if c.kernel == L.APT_KERNEL_MMA_SPLITK:
-        assert c.bm == 32 and c.bn in (8, 16) and c.bn >= min(M, 16)
-        assert c.split_k == 4 and c.cluster_n == 1
-    elif c.kernel == L.APT_KERNEL_GEMV:
+    assert c.mma_kind == L.APT_MMA_I8
+    if c.kernel == L.APT_KERNEL_GEMV:
         assert M <= 2 and c.bm == 32 and c.bn == M and c.split_k in (8, 16) and c.stages == 1
         assert c.cluster_n == 1 and c.cta_pair == 0
     elif c.kernel == L.APT_KERNEL_SKINNY:
@@ -115,7 +113,11 @@ def test_gemm_argument_errors_before_launch():
     assert _gemm(16, 64, 256, 2, 2, W, A, kind=7) == E
     Wm = _fake_packed(64, 256, 2, addr=0x10004)                     # misaligned planes
     assert _gemm(16, 64, 256, 2, 2, Wm, A) == E
-    bad = L.AptConfig(L.APT_KERNEL_MMA_SPLITK, 2, 2, 32, 24, 256, 2, 4, 0, 1)  # bn 24 illegal
+    bad = L.AptConfig(1, 2, 2, 32, 16, 256, 2, 4, 0, 1, 0)  # kernel 1 (removed in ABI 3)
+    assert _gemm(16, 64, 256, 2, 2, W, A, cfg=bad) == L.APT_ERR_UNSUPPORTED
+    bad = L.AptConfig(L.APT_KERNEL_SKINNY, 2, 2, 16, 24, 256, 1, 8, 0, 1, 0)  # bn 24 illegal
+    assert _gemm(16, 64, 256, 2, 2, W, A, cfg=bad) == L.APT_ERR_UNSUPPORTED
+    bad = L.AptConfig(L.APT_KERNEL_SKINNY, 2, 2, 16, 16, 256, 1, 8, 0, 1, 5)  # unknown mma_kind
     assert _gemm(16, 64, 256, 2, 2, W, A, cfg=bad) == L.APT_ERR_UNSUPPORTED
     Wb, Ab = _fake_packed(64, 40000, 8), _fake_packed(16, 40000, 8)
     assert _gemm(16, 64, 40000, 8, 8, Wb, Ab) == L.APT_ERR_UNSUPPORTED
@@ -142,6 +144,21 @@ def test_no_device_means_cuda_error_not_fallback():
     assert _gemm(16, 64, 256, 2, 2, W, A) == L.APT_ERR_CUDA
     out = L.AptPacked(0, 0, 0, 0, 0x10000, 0x20000, None, L.APT_PACK_ROWS)
     assert L.lib().apt_pack_bipolar(0x1000, 4, 4, 4, 2, 0, ctypes.byref(out), None, None) == L.APT_ERR_CUDA
+
+
+def test_python_pack_validates_out():
+    """A caller-supplied `out` must match the codes' shape/bits exactly (no OOB writes)."""
+    import paper_2508_19087_b200 as P
+    from paper_2508_19087_b200 import api
+    out = api.Packed(torch.zeros((2, 4, 8), dtype=torch.int32), torch.zeros(4, dtype=torch.int32), 4, 256, 2)
+    api._check_out(out, 4, 256, 2, False, False)
+    for args in ((4, 256, 3), (5, 256, 2), (4, 300, 2)):
+        with pytest.raises(ValueError):
+            api._check_out(out, *args, False, False)
+    with pytest.raises(ValueError):
+        api._check_out(out, 4, 256, 2, True, False)      # tiled buffers need 128-row padding
+    with pytest.raises(ValueError):
+        api._check_out(out, 4, 256, 2, False, True)      # digit view requested but absent
 
 
 def test_python_api_refuses_cpu_tensors():

@@ -158,28 +158,58 @@ def test_bound_rejected():
         P.gemm(W, A)
 
 
-@pytest.mark.parametrize("bn", [8, 16])
-def test_config_invariance_decode(bn):
-    """any legal configuration gives identical bits (decode kernel token tile)."""
-    a = signed_codes(20, 4096, 4, seed=3)
-    w = signed_codes(200, 4096, 3, seed=4)
-    cfg = dict(P.select_config(20, 200, 4096, 3, 4), kernel=1, bm=32, bk=256, bn=bn, split_k=4, stages=2,
-               cluster_n=1)
-    _check_gemm(a, 4, w, 3, config=cfg, tiled=False)
+def _family_cfgs(m, n, k, wb, ab):
+    """One legal configuration of every kernel family for an M <= 4 problem."""
+    base = P.select_config(m, n, k, wb, ab)
+    return {
+        "gemv": dict(base, kernel=3, bm=32, bn=m, bk=128, split_k=8, stages=1, cta_pair=0, cluster_n=1),
+        "skinny": dict(base, kernel=4, bm=16, bn=8, bk=256, split_k=8, stages=1, cta_pair=0, cluster_n=1),
+        "tc": dict(base, kernel=2, bm=128, bn=16, bk=128, split_k=2, stages=_tc_stages(wb, 16), cta_pair=0,
+                   cluster_n=1),
+    }
 
 
-def test_decode_vs_tc_same_bits():
-    """The decode (mma.sync) and prefill (tcgen05) kernels agree bit for bit on one problem."""
-    a = signed_codes(40, 3000, 6, seed=8)
-    w = signed_codes(333, 3000, 5, seed=9)
-    A, W = _pack_both(a, 6, w, 5, tiled=False)
-    ct = P.select_config(40, 333, 3000, 5, 6)
-    cd = dict(ct, kernel=1, bm=32, bk=256, bn=16, split_k=4, stages=2, cluster_n=1)
-    assert ct["kernel"] == 2
-    y1 = P.gemm(W, A, config=cd).cpu().numpy()
-    y2 = P.gemm(W, A, config=ct).cpu().numpy()
-    assert np.array_equal(y1, y2)
-    assert np.array_equal(y1.astype(np.int64), O.gemm_signed(a, w))
+@pytest.mark.parametrize("wb,ab", [(3, 4), (1, 2), (8, 8)])
+def test_config_invariance_families(wb, ab):
+    """the GEMV, skinny mma.sync and tcgen05 kernels agree bit for bit on one problem (and
+    with the oracle)."""
+    m, n, k = 3, 333, 3000
+    a = signed_codes(m, k, ab, seed=8 + wb)
+    w = signed_codes(n, k, wb, seed=9 + ab)
+    A = P.pack(_dev(a), ab, digits=True)
+    W = P.pack(_dev(w), wb, tiled=True)
+    ref = O.gemm_signed(a, w)
+    for name, cfg in _family_cfgs(m, n, k, wb, ab).items():
+        got = P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, ref), name
+
+
+# ----------------------------------------------------------------------------- stream order (PDL)
+
+@pytest.mark.parametrize("family", ["gemv", "skinny", "tc", "auto16"])
+def test_repack_same_buffer_stream_order(family):
+    """Stream order under programmatic dependent launch (include/apt.h "General contract"): pack W1
+    into a buffer, GEMM, re-pack DIFFERENT codes W2 into the SAME buffer and GEMM immediately on one
+    stream, 50 times, no host synchronisation in between.  Every GEMM must see the weights packed
+    just before it (the GEMMs read weight planes / row sums / scales before griddepcontrol.wait)."""
+    n, k = 28672, 4096  # the pack spans many waves
+    m = 16 if family == "auto16" else 3
+    wb, ab = 3, 4
+    a = signed_codes(m, k, ab, seed=1)
+    w1 = signed_codes(n, k, wb, seed=2)
+    w2 = signed_codes(n, k, wb, seed=3)
+    y1, y2 = c_gemm_i64(a, w1), c_gemm_i64(a, w2)
+    A = P.pack(_dev(a), ab, digits=True)
+    cfg = None if family == "auto16" else _family_cfgs(m, n, k, wb, ab)[family]
+    d1, d2 = _dev(w1), _dev(w2)
+    W = P.alloc_packed(n, k, wb, DEV, tiled=True)
+    outs = []
+    for it in range(50):
+        P.pack(d1 if it % 2 == 0 else d2, wb, out=W)
+        outs.append(P.gemm(W, A, config=cfg))
+    torch.cuda.synchronize()
+    for it, o in enumerate(outs):
+        assert np.array_equal(o.cpu().numpy().astype(np.int64), y1 if it % 2 == 0 else y2), it
 
 
 def _tc_stages(wb, bn):
