@@ -26,8 +26,10 @@
  *     GEMM's weights stream from HBM while the previous kernel finishes; activation-side operands
  *     and the output are touched only after the wait.  This is safe whenever the kernel that wrote the
  *     weight-side buffers did not release its dependents early: apt_pack_bipolar / apt_quantize_pack
- *     never do (their dependents start after every CTA has exited, stores fenced at GPU scope), and
- *     ordinary kernels (torch, cuBLAS, memcpy) never do.  Only a caller kernel that itself executes
+ *     without a digit view never do (their dependents start after every CTA has exited, stores
+ *     fenced at GPU scope), and ordinary kernels (torch, cuBLAS, memcpy) never do.  A pack WITH a
+ *     digit view produces an activation operand and releases its dependents at entry (activations
+ *     are read after the wait); apt_gemm therefore rejects a W that carries a digit view.  Only a caller kernel that itself executes
  *     griddepcontrol.launch_dependents / cudaTriggerProgrammaticLaunchCompletion BEFORE writing the
  *     weights of the apt_gemm that follows it on the same stream breaks this; insert an event or
  *     any non-PDL kernel between them.
@@ -240,7 +242,8 @@ APT_API size_t apt_gemm_zp_workspace_bytes(const apt_config* cfg, int32_t M, int
  *   cfg       : host, NULL -> apt_select_config.
  *   workspace : device scratch of apt_gemm_workspace_bytes(cfg, M, N, K) bytes (nullable if 0).
  * Bound (reading Q8): requires Kpad * (2^abits - 1) * (2^wbits - 1) < 2^31, else APT_ERR_UNSUPPORTED.
- * Errors: APT_ERR_INVALID_ARGUMENT, APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ERR_CUDA. */
+ * Errors: APT_ERR_INVALID_ARGUMENT (also: W->digits != NULL, see "General contract"),
+ *         APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ERR_CUDA. */
 APT_API apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, const apt_packed* W,
                     const apt_packed* A, const apt_scales* scales, apt_out_kind kind, apt_layout layout,
                     void* out, int64_t ldo, const apt_config* cfg, void* workspace, size_t ws_bytes,

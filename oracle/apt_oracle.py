@@ -214,6 +214,23 @@ def gemm_signed(a_codes: np.ndarray, w_codes: np.ndarray) -> np.ndarray:
     return a @ w.T
 
 
+def gemm_signed_blas(a_codes: np.ndarray, w_codes: np.ndarray, chunk: int = 4096) -> np.ndarray:
+    """The same plain definition Y = A . W^T evaluated with a library fp64 matmul (BLAS dgemm) as
+    the one step, for full-size outputs (BASELINE configs[2]-[4], up to 4096 x 28672 x 8192) that
+    the int64 loops cannot finish in seconds.  Exact: every product |a w| <= 2^14 and every partial
+    sum, in whatever order BLAS adds, is an integer of magnitude <= K * 2^14 < 2^53, so each fp64
+    operation is exact and the result equals the int64 GEMM bit for bit (asserted for K < 2^39).
+    W is processed in row chunks to bound host memory."""
+    a = np.asarray(a_codes)
+    w = np.asarray(w_codes)
+    assert a.shape[1] == w.shape[1] and a.shape[1] < (1 << 39)
+    af = a.astype(np.float64)
+    out = np.empty((a.shape[0], w.shape[0]), dtype=np.int64)
+    for n0 in range(0, w.shape[0], chunk):
+        out[:, n0:n0 + chunk] = (af @ w[n0:n0 + chunk].astype(np.float64).T).astype(np.int64)
+    return out
+
+
 def gemm_python(a_rows, w_rows) -> list[list[int]]:
     """Arbitrary-precision Python-int triple loop ("second independent
     implementation"); tiny inputs only."""

@@ -261,6 +261,9 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
     return APT_ERR_INVALID_ARGUMENT;
   apt_status st = validate_packed(W, N, K, wbits);
   if (st != APT_OK) return st;
+  // a packed matrix with a digit view is an activation operand (its pack releases dependents early,
+  // include/apt.h "General contract"); it may not serve as the weight operand
+  if (W->digits) return APT_ERR_INVALID_ARGUMENT;
   st = validate_packed(A, M, K, abits);
   if (st != APT_OK) return st;
   if (kind != APT_OUT_I32_SIGNED && kind != APT_OUT_I32_BIPOLAR && kind != APT_OUT_F16_SCALED)

@@ -66,6 +66,70 @@ __host__ __device__ __forceinline__ void rebuild8(const uint32_t* w, uint32_t (&
   }
 }
 
+// The inverse of rebuild8<Q> (the pack direction): 8 registers of digits in rebuild8's slot order
+// -> Q plane words (element c -> bit c).  bf_pair is an involution for a fixed (s, m), so the
+// inverse is the same butterfly run backwards.  Digits must be < 2^Q.
+template <int Q>
+__host__ __device__ __forceinline__ void unbuild8(const uint32_t (&o)[8], uint32_t* w) {
+  static_assert(Q >= 1 && Q <= 8, "bits");
+  if constexpr (Q <= 4) {
+    uint32_t g[4], e01, f01, e23, f23;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) g[c] = o[2 * c] | (o[2 * c + 1] << 4);
+    bf_pair(g[0], g[1], 2, 0x33333333u, e01, e23);
+    bf_pair(g[2], g[3], 2, 0x33333333u, f01, f23);
+    uint32_t w0, w1, w2, w3;
+    bf_pair(e01, f01, 1, 0x55555555u, w0, w1);
+    bf_pair(e23, f23, 1, 0x55555555u, w2, w3);
+    w[0] = w0;
+    if (Q >= 2) w[1] = w1;
+    if (Q >= 3) w[2] = w2;
+    if (Q >= 4) w[3] = w3;
+  } else {
+    uint32_t g[8], e01, f01, e23, f23, e45, f45, e67, f67, x[8];
+    bf_pair(o[0], o[1], 4, 0x0F0F0F0Fu, g[0], g[2]);
+    bf_pair(o[2], o[3], 4, 0x0F0F0F0Fu, g[1], g[3]);
+    bf_pair(o[4], o[5], 4, 0x0F0F0F0Fu, g[4], g[6]);
+    bf_pair(o[6], o[7], 4, 0x0F0F0F0Fu, g[5], g[7]);
+    bf_pair(g[0], g[1], 2, 0x33333333u, e01, e23);
+    bf_pair(g[2], g[3], 2, 0x33333333u, e45, e67);
+    bf_pair(g[4], g[5], 2, 0x33333333u, f01, f23);
+    bf_pair(g[6], g[7], 2, 0x33333333u, f45, f67);
+    bf_pair(e01, f01, 1, 0x55555555u, x[0], x[1]);
+    bf_pair(e23, f23, 1, 0x55555555u, x[2], x[3]);
+    bf_pair(e45, f45, 1, 0x55555555u, x[4], x[5]);
+    bf_pair(e67, f67, 1, 0x55555555u, x[6], x[7]);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) w[i] = x[i];
+  }
+}
+
+__host__ __device__ __forceinline__ uint32_t byte_perm(uint32_t a, uint32_t b, uint32_t sel) {
+#ifdef __CUDA_ARCH__
+  return __byte_perm(a, b, sel);
+#else
+  const uint64_t v = ((uint64_t)b << 32) | a;
+  uint32_t r = 0;
+  for (int i = 0; i < 4; ++i) r |= (uint32_t)((v >> (8 * ((sel >> (4 * i)) & 7))) & 0xFF) << (8 * i);
+  return r;
+#endif
+}
+
+// 32 digits in natural order (register i byte c = element 4i + c) -> rebuild8's slot order
+// (register j byte b = element 8b + rev3(j)): two 4 x 4 byte transposes, 16 PRMT.
+__host__ __device__ __forceinline__ void to_slot_order(const uint32_t (&n)[8], uint32_t (&o)[8]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t t0 = byte_perm(n[h], n[2 + h], 0x5140u), t1 = byte_perm(n[h], n[2 + h], 0x7362u);
+    const uint32_t t2 = byte_perm(n[4 + h], n[6 + h], 0x5140u), t3 = byte_perm(n[4 + h], n[6 + h], 0x7362u);
+    // column c of the transpose holds elements 8b + 4h + c; slot register rev3(4h + c)
+    o[h ? 1 : 0] = byte_perm(t0, t2, 0x5410u);
+    o[h ? 5 : 4] = byte_perm(t0, t2, 0x7632u);
+    o[h ? 3 : 2] = byte_perm(t1, t3, 0x5410u);
+    o[h ? 7 : 6] = byte_perm(t1, t3, 0x7632u);
+  }
+}
+
 // Runtime-width dispatch (used where the width is not a template parameter, e.g. token rebuild).
 __host__ __device__ __forceinline__ void rebuild8_rt(const uint32_t* w, int q, uint32_t (&o)[8]) {
   switch (q) {

@@ -36,6 +36,19 @@ static int check(int ref_slot[32]) {
     uint32_t o2[8];
     apt::rebuild8_rt(w, Q, o2);
     for (int r = 0; r < 8; ++r) if (o2[r] != o[r]) ++bad;
+    // the pack direction: unbuild8 inverts rebuild8 exactly
+    uint32_t back[8] = {0};
+    apt::unbuild8<Q>(o, back);
+    for (int i = 0; i < Q; ++i) if (back[i] != w[i]) ++bad;
+    // natural-order digits -> slot order == rebuild8's slots
+    uint32_t nat[8] = {0}, so[8];
+    for (int e = 0; e < 32; ++e) {
+      uint32_t u = 0;
+      for (int i = 0; i < Q; ++i) u |= ((w[i] >> e) & 1u) << i;
+      nat[e / 4] |= u << (8 * (e % 4));
+    }
+    apt::to_slot_order(nat, so);
+    for (int r = 0; r < 8; ++r) if (so[r] != o[r]) ++bad;
   }
   return bad;
 }

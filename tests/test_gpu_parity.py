@@ -297,17 +297,34 @@ def test_llama7b_decode_full(n, k, m, pw, pa):
 
 
 @pytest.mark.parametrize("n,k", LLAMA7B)
+@pytest.mark.parametrize("m", [1, 8, 16])
+@pytest.mark.parametrize("pw,pa", [(1, 2), (2, 2), (3, 4), (4, 4)])
+def test_llama7b_decode_full_f16(n, k, m, pw, pa):
+    """The bench's exact call at every BASELINE configs[1] shape: fp16 output with per-channel
+    w_scale and per-token a_scale (selector default config), every element within 1e-3 of the
+    fp64-scaled oracle (reading Q10/Q14)."""
+    a = signed_codes(m, k, pa, seed=config_seed(1, pw, pa, salt=7))
+    w = signed_codes(n, k, pw, seed=config_seed(1, pw, pa, salt=7) + 1)
+    ws = log_uniform_scales(n, -10, -6, seed=n + pw)
+    as_ = log_uniform_scales(m, -6, -2, seed=m + pa)
+    A = P.pack(_dev(a), pa, digits=True)
+    W = P.pack(_dev(w), pw, tiled=True)
+    got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_)).cpu().numpy().astype(np.float64)
+    ref = O.scale_fp64(c_gemm_i64(a, w), ws, as_)
+    assert (np.abs(got - ref) <= 1e-3 * np.abs(ref) + 2.0 ** -24).all()
+
+
+@pytest.mark.parametrize("n,k", LLAMA7B)
 @pytest.mark.parametrize("pw,pa", [(2, 8), (4, 4)])
-def test_llama7b_prefill_sampled(n, k, pw, pa):
-    """BASELINE configs[2] (M=2048) at full size: 16 sampled token rows vs the C oracle, plus a
-    property that holds at any size (row sums of Y = A . (sum of W rows))."""
+def test_llama7b_prefill_full(n, k, pw, pa):
+    """BASELINE configs[2] (M=2048) at full size in the selector's launch configuration: EVERY
+    output element vs the oracle (gemm_signed_blas, exact), plus the row-sum identity."""
     m = 2048
     a = signed_codes(m, k, pa, seed=config_seed(2, pw, pa))
     w = signed_codes(n, k, pw, seed=config_seed(2, pw, pa) + 1)
     A, W = _pack_both(a, pa, w, pw)
     got = P.gemm(W, A).cpu().numpy().astype(np.int64)
-    rows = np.random.default_rng(0).choice(m, 16, replace=False)
-    assert np.array_equal(got[rows], c_gemm_i64(a[rows], w))
+    assert np.array_equal(got, O.gemm_signed_blas(a, w))
     wsum = w.astype(np.int64).sum(0)
     assert np.array_equal(got.sum(1), a.astype(np.int64) @ wsum)
 
@@ -425,46 +442,38 @@ def test_gemv_llama7b_full(n, k, pw, pa):
 
 # ----------------------------------------------------------------------------- configs[3], configs[4] at full size
 
-def _sampled_check(got, a, w, rows):
-    assert np.array_equal(got[rows], c_gemm_i64(a[rows], w))
-    wsum = w.astype(np.int64).sum(0)
-    assert np.array_equal(got.sum(1), a.astype(np.int64) @ wsum)
-
-
 @pytest.mark.parametrize("n,k", [(8192, 8192), (28672, 8192)])
-def test_llama70b_sampled_and_tp_slices(n, k):
+def test_llama70b_full_and_tp_slices(n, k):
     """BASELINE configs[3] (Llama-3-70B linears, M = 4096, W2A4) at full size in the selector's launch
-    configuration: 8 sampled token rows vs the C oracle, the row-sum identity over all rows, and the
-    N-split tensor-parallel slices (P = 8, column layout, as each rank computes them) concatenate to
-    the single-GPU result bit for bit."""
+    configuration: EVERY output element vs the oracle (gemm_signed_blas, exact), and the N-split
+    tensor-parallel slices (P = 8, column layout, as each rank computes them) concatenate to the
+    single-GPU result bit for bit."""
     m, pw, pa = 4096, 2, 4
     a = signed_codes(m, k, pa, seed=config_seed(3, pw, pa))
     w = signed_codes(n, k, pw, seed=config_seed(3, pw, pa) + 1)
     A, W = _pack_both(a, pa, w, pw)
     full = P.gemm(W, A)
-    got = full.cpu().numpy().astype(np.int64)
-    _sampled_check(got, a, w, np.random.default_rng(3).choice(m, 8, replace=False))
+    assert np.array_equal(full.cpu().numpy().astype(np.int64), O.gemm_signed_blas(a, w))
     p = 8
     rows = n // p
-    for r in (0, p - 1):
+    for r in range(p):
         Wr = P.pack(_dev(w[r * rows:(r + 1) * rows]), pw, tiled=True)
         yt = P.gemm(Wr, A, layout="col")  # [rows, M] = the rank's block of Y^T
         assert torch.equal(yt.t(), full[:, r * rows:(r + 1) * rows])
 
 
 @pytest.mark.parametrize("pw", range(1, 9))
-def test_sweep_4096_cube_sampled(pw):
+def test_sweep_4096_cube_full(pw):
     """BASELINE configs[4]: 4096^3 for every (p_w, p_a) in 1..8 x 1..8 with the selector's config,
-    4 sampled token rows vs the C oracle plus the row-sum identity."""
+    EVERY output element vs the oracle (gemm_signed_blas, exact)."""
     n = m = k = 4096
     w = signed_codes(n, k, pw, seed=config_seed(4, pw, 0))
     W = P.pack(_dev(w), pw, tiled=True)
-    rows = np.random.default_rng(pw).choice(m, 4, replace=False)
     for pa in range(1, 9):
         a = signed_codes(m, k, pa, seed=config_seed(4, pw, pa))
         A = P.pack(_dev(a), pa, digits=True)
-        got = P.gemm(W, A).cpu().numpy().astype(np.int64)
-        _sampled_check(got, a, w, rows)
+        got = P.gemm(W, A).cpu().numpy()
+        assert np.array_equal(got.astype(np.int64), O.gemm_signed_blas(a, w)), pa
 
 
 # ----------------------------------------------------------------------------- mma.sync skinny GEMM (M <= 16)

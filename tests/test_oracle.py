@@ -276,6 +276,28 @@ def test_c_oracle_matches_library_and_bigint():
             assert got.tolist() == O.gemm_python(a.tolist(), w.tolist())
 
 
+def test_blas_oracle_exact():
+    """gemm_signed_blas (fp64 BLAS as the one step) equals the C int64 loop and the Python big-int
+    loop bit for bit: random shapes and precisions, chunk boundaries, the all-minimum W8A8 edge at
+    K = 33024 (|Y| = K 2^14, every partial sum an exact fp64 integer), and alternating signs."""
+    rng = np.random.default_rng(11)
+    for t in range(12):
+        m, n, k = (int(v) for v in rng.integers(1, 90, size=3))
+        pa, pw = (int(v) for v in rng.integers(1, 9, size=2))
+        a = signed_codes(m, k, pa, seed=500 + t)
+        w = signed_codes(n, k, pw, seed=600 + t)
+        got = O.gemm_signed_blas(a, w, chunk=7)
+        assert got.dtype == np.int64 and (got == c_gemm_i64(a, w)).all()
+        if t < 2:
+            assert got.tolist() == O.gemm_python(a.tolist(), w.tolist())
+    k = 33024
+    a = np.full((2, k), -128, dtype=np.int8)
+    w = np.full((3, k), -128, dtype=np.int8)
+    assert (O.gemm_signed_blas(a, w) == k * 2 ** 14).all()
+    a[:, ::2] = 127
+    assert (O.gemm_signed_blas(a, w) == c_gemm_i64(a, w)).all()
+
+
 def test_scale_fp64_within_two_roundings():
     rng = np.random.default_rng(5)
     y = rng.integers(-(1 << 30), 1 << 30, size=(4, 6))
