@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define APT_ABI_VERSION 3
+#define APT_ABI_VERSION 4
 #define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
 
 typedef enum {
@@ -188,10 +188,19 @@ typedef enum {
   APT_KERNEL_GEMV = 3,       /* M <= 4: SIMT GEMV, weights rebuilt in registers (same u8 digits), dp4a
                                 against the activation digit view; 32 weight rows x all of K per CTA
                                 (bm = 32, bn = M, bk = 128, split_k = 8 or 16 warps, stages = 1)  */
-  APT_KERNEL_SKINNY = 4      /* M <= 16 per token tile: mma.sync m16n8k32 u8 fed from registers (weights
+  APT_KERNEL_SKINNY = 4,     /* M <= 16 per token tile: mma.sync m16n8k32 u8 fed from registers (weights
                                 rebuilt in registers, tokens from the digit view), 16 weight rows x
                                 bn (8 or 16) tokens x all of K per CTA (bm = 16, bk = 256,
                                 split_k = 4, 8 or 16 warps splitting K, stages = 1)                */
+  APT_KERNEL_DEC = 5         /* M <= 16: mma.sync m16n8k32 u8 with the WEIGHTS as the streamed B operand
+                                (8 rows x 32 K per instruction) and the tokens as the A operand (held in
+                                registers, loaded from a per-CTA shared-memory slab); weights copied into a
+                                per-lane shared-memory ring with cp.async.  bm = 128 weight rows per CTA of
+                                4 warps, bn = 8 (M <= 8) or 16, bk = 256, stages = ring depth (16 for
+                                wbits <= 2, 8 for 3-4, 4 above), split_k = CTAs along K (1..32, at most
+                                16 blocks of 256 K per CTA; > 1 uses the workspace: int32 partials + one
+                                ticket per row tile, see apt_gemm_workspace_bytes).  Needs
+                                Kpad * 255 * 255 < 2^32 (digits are rebuilt as u * 2^s). */
 } apt_kernel;
 
 /* Kernel configuration (the B200 analogue of the paper's tunable hyperparameters, §5.1).
@@ -227,7 +236,16 @@ typedef struct {
 APT_API apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits,
                              apt_config* out /* host */);
 
-/* Host.  Device workspace bytes apt_gemm needs for (cfg, M, N, K).  0 = none. */
+/* Host.  Device workspace bytes apt_gemm needs for (cfg, M, N, K).
+ * Layout: [APT_WS_TICKET_BYTES of split-K tickets at offset 0 — the same place for every call]
+ * [token digit expansion, M * Kpad bytes, used when the activation operand has no digit view]
+ * [APT_KERNEL_DEC split-K int32 partials].  The ticket area must be ZERO before a workspace is first used
+ * (e.g. one cudaMemsetAsync after allocation); every apt_gemm call leaves it zero again, so one workspace
+ * serves any sequence of calls on a stream.  Calls that may run concurrently (different streams) need
+ * distinct workspaces.  A call that needs no workspace (digit-view activations, no split-K, no zero
+ * points) accepts NULL. */
+#define APT_WS_TICKETS 4096
+#define APT_WS_TICKET_BYTES (APT_WS_TICKETS * 4)
 APT_API size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K);
 
 /* Host.  Device workspace bytes apt_gemm needs for (cfg, M, N, K) when the scales carry zero points

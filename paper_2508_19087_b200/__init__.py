@@ -7,7 +7,7 @@ Public API (torch tensors in, CUDA kernels of libapt.so underneath):
     select_config(M, N, K, wbits, abits) -> kernel configuration       (apt_select_config)
     tp.TPLinear / tp.tp_gemm             -> N-split tensor parallel GEMM + all-gather
 """
-from .api import Packed, alloc_packed, gemm, kpad, pack, quantize_pack, select_config, workspace_bytes  # noqa: F401
+from .api import Packed, alloc_packed, gemm, kpad, pack, quantize_pack, select_config, workspace_bytes, default_workspace  # noqa: F401
 from . import _lib  # noqa: F401
 
-__all__ = ["Packed", "alloc_packed", "gemm", "kpad", "pack", "quantize_pack", "select_config", "workspace_bytes"]
+__all__ = ["Packed", "alloc_packed", "gemm", "kpad", "pack", "quantize_pack", "select_config", "workspace_bytes", "default_workspace"]

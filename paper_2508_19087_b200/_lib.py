@@ -14,9 +14,9 @@ APT_OK, APT_ERR_INVALID_ARGUMENT, APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ER
 APT_ENC_SIGNED, APT_ENC_BIPOLAR = 0, 1
 APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
 APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
-APT_KERNEL_AUTO, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY = 0, 2, 3, 4
+APT_KERNEL_AUTO, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY, APT_KERNEL_DEC = 0, 2, 3, 4, 5
 APT_MMA_I8 = 0
-ABI_VERSION = 3  # include/apt.h APT_ABI_VERSION this binding marshals for
+ABI_VERSION = 4  # include/apt.h APT_ABI_VERSION this binding marshals for
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes", "apt_gemm_zp_workspace_bytes",

@@ -147,6 +147,22 @@ def quantize_pack(x: torch.Tensor, bits: int, out: Packed | None = None, scale: 
     return out, scale
 
 
+_WS = {}
+
+
+def default_workspace(device, nbytes: int) -> torch.Tensor:
+    """The per-device default apt_gemm workspace: zero-filled when (re)allocated, because the split-K
+    tickets inside it must start at zero (apt_gemm leaves them zero).  Calls on one device share it,
+    so concurrent streams must pass their own ``workspace``."""
+    dev = torch.device(device)
+    key = (dev.type, dev.index if dev.index is not None else torch.cuda.current_device())
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros((max(nbytes, 1 << 20),), dtype=torch.uint8, device=dev)
+        _WS[key] = ws
+    return ws
+
+
 def select_config(M: int, N: int, K: int, wbits: int, abits: int) -> dict:
     """apt_select_config (p = wbits, q = abits)."""
     c = L.AptConfig()
@@ -196,17 +212,20 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
                     raise ValueError(f"{nm} must be contiguous fp32")
         sc = L.AptScales(*(t.data_ptr() if t is not None else None for t in (w_scale, a_scale, w_zero, a_zero)))
     c = _config_struct(config)
-    ws_need = 0
     zp = kind == L.APT_OUT_F16_SCALED and (w_zero is not None or a_zero is not None)
-    if A.digits is None or zp:  # digit view expanded into the workspace / int32 Y for the zero points
-        cc = c
-        if cc is None:
-            cc = L.AptConfig()
-            L.check("apt_select_config", L.lib().apt_select_config(M, N, K, W.bits, A.bits, ctypes.byref(cc)))
-        fn = L.lib().apt_gemm_zp_workspace_bytes if zp else L.lib().apt_gemm_workspace_bytes
-        ws_need = int(fn(ctypes.byref(cc), M, N, K))
+    cc = c
+    if cc is None:
+        cc = L.AptConfig()
+        L.check("apt_select_config", L.lib().apt_select_config(M, N, K, W.bits, A.bits, ctypes.byref(cc)))
+    fn = L.lib().apt_gemm_zp_workspace_bytes if zp else L.lib().apt_gemm_workspace_bytes
+    ws_need = int(fn(ctypes.byref(cc), M, N, K))
+    if A.digits is not None and not zp and cc.kernel != L.APT_KERNEL_DEC:
+        ws_need = 0  # the digit view replaces the token expansion area
     if ws_need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < ws_need):
-        workspace = torch.empty((ws_need,), dtype=torch.uint8, device=W.planes.device)
+        if workspace is not None:
+            raise ValueError(f"workspace holds {workspace.numel() * workspace.element_size()} bytes, "
+                             f"apt_gemm needs {ws_need}")
+        workspace = default_workspace(W.planes.device, ws_need)
     ws_ptr = workspace.data_ptr() if workspace is not None else None
     ws_len = workspace.numel() * workspace.element_size() if workspace is not None else 0
     ws, as_ = W.struct(), A.struct()

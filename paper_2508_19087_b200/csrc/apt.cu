@@ -73,6 +73,15 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
     if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
     return APT_OK;
   }
+  if (c->kernel == APT_KERNEL_DEC) {
+    if (M > 16 || c->bm != 32 || c->bn != (M <= 8 ? 8 : 16) || c->bk != 256) return APT_ERR_UNSUPPORTED;
+    if ((c->stages != 4 && c->stages != 8) || c->split_k < 1 || c->split_k > 32) return APT_ERR_UNSUPPORTED;
+    if (c->cta_pair != 0 || c->cluster_n != 1) return APT_ERR_UNSUPPORTED;
+    // 1-4-bit weight digits are u * 2^s (gemm_dec.cu): the unsigned sum must stay below 2^32
+    if (kpad_of(K) * 255ll * 255ll >= (1ll << 32)) return APT_ERR_UNSUPPORTED;
+    if ((N + c->bm - 1) / c->bm > APT_WS_TICKETS) return APT_ERR_UNSUPPORTED;  // one ticket per row tile
+    return APT_OK;
+  }
   if (c->kernel == APT_KERNEL_TC) {
     if (c->bm != 128 || c->bk != 128) return APT_ERR_UNSUPPORTED;
     if (c->bn != 16 && c->bn != 64 && c->bn != 128 && c->bn != 256) return APT_ERR_UNSUPPORTED;
@@ -241,11 +250,18 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
   return APT_OK;
 }
 
+// workspace areas (include/apt.h apt_gemm_workspace_bytes), offsets fixed per (cfg, M, N, K):
+// [split-K tickets, APT_WS_TICKETS uint32, the same place for every call][token digit expansion]
+// [DEC split-K partials]
+static size_t ws_expand_bytes(int32_t M, int32_t K) { return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32)); }
+static size_t ws_dec_off(int32_t M, int32_t K) { return APT_WS_TICKET_BYTES + (ws_expand_bytes(M, K) + 15) / 16 * 16; }
+static size_t ws_dec_bytes(const apt_config* cfg, int32_t N) {
+  return cfg->kernel == APT_KERNEL_DEC ? apt::dec_workspace_bytes(N, cfg->split_k) : 0;
+}
+
 size_t apt_gemm_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
-  // TC kernel: activation digit view for activations packed without one (apt_packed.digits == NULL)
-  (void)N;
-  if (!cfg || M <= 0 || K <= 0) return 0;
-  return apt::tc_workspace_bytes(M, (int)(kpad_of(K) / 32));
+  if (!cfg || M <= 0 || N <= 0 || K <= 0) return 0;
+  return ws_dec_off(M, K) + ws_dec_bytes(cfg, N);
 }
 
 size_t apt_gemm_zp_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, int32_t K) {
@@ -281,7 +297,8 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   }
   st = validate_config(&c, M, N, K, wbits, abits);
   if (st != APT_OK) return st;
-  const size_t need0 = A->digits ? 0 : apt_gemm_workspace_bytes(&c, M, N, K);
+  const size_t dec_ws = ws_dec_bytes(&c, N);
+  const size_t need0 = dec_ws ? ws_dec_off(M, K) + dec_ws : (A->digits ? 0 : APT_WS_TICKET_BYTES + ws_expand_bytes(M, K));
   // zero points (NEXT-2): exact int32 Y into the workspace after the digit-expansion area, then the
   // elementwise zero-point epilogue
   const bool zp = kind == APT_OUT_F16_SCALED && (scales->w_zero || scales->a_zero);
@@ -341,10 +358,10 @@ apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_pa
   const uint8_t* adig = A->digits;
   if (!adig && A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
   if (!adig) {
-    cudaError_t err = apt::launch_expand_tokens(A->planes, (int64_t)M * A->k_words, M, A->k_words, abits,
-                                                reinterpret_cast<uint8_t*>(workspace), s);
+    uint8_t* xp = reinterpret_cast<uint8_t*>(workspace) + APT_WS_TICKET_BYTES;
+    cudaError_t err = apt::launch_expand_tokens(A->planes, (int64_t)M * A->k_words, M, A->k_words, abits, xp, s);
     if (err != cudaSuccess) return APT_ERR_CUDA;
-    adig = reinterpret_cast<const uint8_t*>(workspace);
+    adig = xp;
   }
   if (c.kernel == APT_KERNEL_GEMV || c.kernel == APT_KERNEL_SKINNY) {
     apt::GemvArgs p;
@@ -356,6 +373,23 @@ apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_pa
     p.e = e;
     cudaError_t err = c.kernel == APT_KERNEL_GEMV ? apt::launch_gemv(p, wbits, c.split_k, s)
                                                   : apt::launch_gemm_skinny(p, wbits, c.bn, c.split_k, s);
+    return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+  }
+  if (c.kernel == APT_KERNEL_DEC) {
+    apt::DecArgs p;
+    p.wp = W->planes;
+    p.w_tiled = W->layout == APT_PACK_TILED ? 1 : 0;
+    p.w_pstride = (int64_t)(p.w_tiled ? (N + 127) / 128 * 128 : N) * W->k_words;
+    p.adig = adig;
+    p.k_words = W->k_words;
+    p.e = e;
+    p.partials = nullptr;
+    p.counters = nullptr;
+    if (c.split_k > 1) {
+      p.partials = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(workspace) + ws_dec_off(M, e.K));
+      p.counters = reinterpret_cast<uint32_t*>(workspace);
+    }
+    cudaError_t err = apt::launch_gemm_dec(p, wbits, c.stages, c.split_k, s);
     return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   if (c.kernel == APT_KERNEL_TC) {

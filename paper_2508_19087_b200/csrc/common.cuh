@@ -20,11 +20,22 @@ namespace apt {
 //
 // Cost (after constant folding): about 20 ops for Q <= 2, 28 for Q = 4, 48 for Q = 8 per 32 elements.
 // ---------------------------------------------------------------------------------------------
+// (x & m) | (y & ~m) as ONE lop3 on the device (the compiler tends to emit two)
+__host__ __device__ __forceinline__ uint32_t bit_select(uint32_t x, uint32_t y, uint32_t m) {
+#ifdef __CUDA_ARCH__
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(x), "r"(y), "r"(m));
+  return d;
+#else
+  return (x & m) | (y & ~m);
+#endif
+}
+
 __host__ __device__ __forceinline__ void bf_pair(uint32_t lo, uint32_t hi, int s, uint32_t m, uint32_t& a, uint32_t& b) {
   // a: even fields of lo in the low half, even fields of hi in the high half (field width s)
   // b: odd fields likewise.  m = mask of the low s bits of every 2s-bit field.
-  a = (lo & m) | ((hi << s) & ~m);
-  b = ((lo >> s) & m) | (hi & ~m);
+  a = bit_select(lo, hi << s, m);
+  b = bit_select(lo >> s, hi, m);
 }
 
 // The element -> byte-slot bijection is the SAME for every Q (planes >= Q are zero and the
@@ -63,6 +74,57 @@ __host__ __device__ __forceinline__ void rebuild8(const uint32_t* w, uint32_t (&
     bf_pair(g[1], g[3], 4, 0x0F0F0F0Fu, o[2], o[3]);
     bf_pair(g[4], g[6], 4, 0x0F0F0F0Fu, o[4], o[5]);
     bf_pair(g[5], g[7], 4, 0x0F0F0F0Fu, o[6], o[7]);
+  }
+}
+
+// rebuild8's slot order is "strided": register j byte b holds element 8b + rev3(j) (rev3 = 3-bit
+// reversal).  For 1- and 2-bit operands that order is cheaper to produce one register at a time with
+// the digit placed in the TOP bits of its byte: register j = each plane shifted so that bit
+// 8b + rev3(j) lands in bit 8 - Q + i of byte b, then masked.  The left shifts compile to IMAD.SHL
+// (FMA pipe), leaving only the masks on the integer ALU pipe (8 LOP3 per word at Q = 1 against ~20
+// for the butterfly).  Every byte is u * 2^(8-Q); the GEMM divides the exact sum by 2^(8-Q).
+__host__ __device__ __forceinline__ constexpr int rev3(int j) { return ((j & 1) << 2) | (j & 2) | ((j >> 2) & 1); }
+
+template <int S>
+__host__ __device__ __forceinline__ uint32_t shl_signed(uint32_t v) {
+  if constexpr (S >= 0) return v << S; else return v >> (-S);
+}
+
+template <int Q>
+__host__ __device__ __forceinline__ void rebuild_hi(const uint32_t* w, uint32_t (&o)[8]) {
+  static_assert(Q == 1 || Q == 2, "rebuild_hi covers 1- and 2-bit operands");
+  if constexpr (Q == 1) {
+    o[0] = shl_signed<7 - rev3(0)>(w[0]) & 0x80808080u;
+    o[1] = shl_signed<7 - rev3(1)>(w[0]) & 0x80808080u;
+    o[2] = shl_signed<7 - rev3(2)>(w[0]) & 0x80808080u;
+    o[3] = shl_signed<7 - rev3(3)>(w[0]) & 0x80808080u;
+    o[4] = shl_signed<7 - rev3(4)>(w[0]) & 0x80808080u;
+    o[5] = shl_signed<7 - rev3(5)>(w[0]) & 0x80808080u;
+    o[6] = shl_signed<7 - rev3(6)>(w[0]) & 0x80808080u;
+    o[7] = shl_signed<7 - rev3(7)>(w[0]) & 0x80808080u;
+  } else {
+#define APT_HI2(j) o[j] = bit_select(shl_signed<6 - rev3(j)>(w[0]), shl_signed<7 - rev3(j)>(w[1]) & 0x80808080u, 0x40404040u)
+    APT_HI2(0); APT_HI2(1); APT_HI2(2); APT_HI2(3); APT_HI2(4); APT_HI2(5); APT_HI2(6); APT_HI2(7);
+#undef APT_HI2
+  }
+}
+
+// rebuild8<Q> for Q = 3, 4 with every digit scaled by 16 (the nibble left in the high half of its
+// byte): the last butterfly stage becomes one mask (+ one FMA-pipe left shift) per register instead of
+// a right shift and a mask on the ALU pipe.  Same slots as rebuild8.
+template <int Q>
+__host__ __device__ __forceinline__ void rebuild_x16(const uint32_t* w, uint32_t (&o)[8]) {
+  static_assert(Q == 3 || Q == 4, "rebuild_x16 covers 3- and 4-bit operands");
+  const uint32_t w3 = (Q >= 4) ? w[3] : 0u;
+  uint32_t e01, f01, e23, f23, g[4];
+  bf_pair(w[0], w[1], 1, 0x55555555u, e01, f01);
+  bf_pair(w[2], w3, 1, 0x55555555u, e23, f23);
+  bf_pair(e01, e23, 2, 0x33333333u, g[0], g[1]);
+  bf_pair(f01, f23, 2, 0x33333333u, g[2], g[3]);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    o[2 * c] = (g[c] << 4) & 0xF0F0F0F0u;
+    o[2 * c + 1] = g[c] & 0xF0F0F0F0u;
   }
 }
 

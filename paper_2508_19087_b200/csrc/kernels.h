@@ -56,6 +56,23 @@ struct GemvArgs {
 cudaError_t launch_gemv(const GemvArgs& p, int wbits, int warps, cudaStream_t stream);  // warps: 8 or 16
 // M <= 16: mma.sync m16n8k32 u8 skinny GEMM fed from registers (gemm_skinny.cu); bn 8 or 16, warps 4/8/16
 cudaError_t launch_gemm_skinny(const GemvArgs& p, int wbits, int bn, int warps, cudaStream_t stream);
+
+// M <= 16: mma.sync m16n8k32 u8 with the weights as the streamed B operand and the tokens resident in
+// registers (gemm_dec.cu); 32 weight rows per CTA of `warps` (4 / 8) warps splitting K, split = CTAs
+// along K (> 1 needs the partials + tickets workspace, tickets zero before the first call and left zero)
+struct DecArgs {
+  const uint32_t* wp;      // weight planes (row or tile-major layout)
+  int64_t w_pstride;       // words per plane
+  int32_t w_tiled;
+  const uint8_t* adig;     // activation digits [M][Kpad], kernel K order
+  int32_t k_words;
+  EpilogueArgs e;
+  int32_t* partials;       // [tiles][split][16][32] int32 (split > 1)
+  uint32_t* counters;      // [tiles] tickets (split > 1)
+};
+cudaError_t launch_gemm_dec(const DecArgs& p, int wbits, int warps, int split, cudaStream_t stream);
+size_t dec_workspace_bytes(int N, int split);
+int dec_blocks_per_cta(int k_words, int split);
 }  // namespace apt
 
 namespace apt {

@@ -63,21 +63,23 @@ __device__ __forceinline__ uint32_t from_offset4(uint32_t u) {
 // scope before exiting.
 __device__ __forceinline__ void pack_release() { __threadfence(); }
 
-// the 128 signed codes of one quad as 32 natural-order words (4 words per 32-element output word)
-template <bool QUANT>
-__device__ __forceinline__ void load_quad(const PackArgs& p, const void* rowp, int c0, float s, int qmax,
-                                          uint32_t (&v)[32]) {
+// the 32 * WPI signed codes of one work item (WPI consecutive 32-element words) as 8 * WPI natural-order
+// words (4 codes each)
+template <bool QUANT, int WPI>
+__device__ __forceinline__ void load_words(const PackArgs& p, const void* rowp, int c0, float s, int qmax,
+                                           uint32_t (&v)[8 * WPI]) {
+  constexpr int kE = 32 * WPI;  // codes per item
   if constexpr (!QUANT) {
     const int8_t* row = reinterpret_cast<const int8_t*>(rowp);
-    if (((reinterpret_cast<uintptr_t>(row) & 15u) == 0) && c0 + 128 <= p.k) {
+    if (((reinterpret_cast<uintptr_t>(row) & 15u) == 0) && c0 + kE <= p.k) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < 2 * WPI; ++j) {
         const uint4 t = __ldg(reinterpret_cast<const uint4*>(row + c0) + j);
         v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
+      for (int j = 0; j < 8 * WPI; ++j) {
         uint32_t word = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -96,9 +98,9 @@ __device__ __forceinline__ void load_quad(const PackArgs& p, const void* rowp, i
   } else {
     // fp16 -> codes: x_hat = clamp(rint(RN_f32(x / s)), -qmax - 1, qmax), 0 where s == 0 (reading R-Q)
     const __half* row = reinterpret_cast<const __half*>(rowp);
-    const bool vec = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0) && c0 + 128 <= p.k;
+    const bool vec = ((reinterpret_cast<uintptr_t>(row) & 15u) == 0) && c0 + kE <= p.k;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < 4 * WPI; ++j) {
       float f[8];
       if (vec) {
         const uint4 t = __ldg(reinterpret_cast<const uint4*>(row + c0) + j);
@@ -128,7 +130,9 @@ __device__ __forceinline__ void load_quad(const PackArgs& p, const void* rowp, i
   }
 }
 
-template <int BITS, bool QUANT>
+// WPI = words per work item: 4 (a 128-element quad, one 16-byte store per plane: the weight packs,
+// bandwidth) or 1 (one 32-element word: the activation packs, a short per-thread critical path)
+template <int BITS, bool QUANT, int WPI>
 __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const __half* __restrict__ x, float* scale,
                                                              int rows_per_cta) {
   if (p.digits) pdl_launch_dependents();  // activation operand: see pack_release()
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
   __shared__ unsigned s_amax[kPackMaxRows];
   const int R = rows_per_cta;
   const int r0 = blockIdx.x * R;
-  const int Q = p.k_words >> 2;  // quads per row
+  const int Q = p.k_words / WPI;  // work items per row
   const int items = R * Q;
   constexpr int kQmax = (1 << (BITS - 1)) - 1;
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
@@ -157,10 +161,10 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
       if (r >= p.rows) continue;
       const __half* row = x + (int64_t)r * p.ld;
       float m = 0.f;
-      const int c0 = 128 * q;
-      if (((reinterpret_cast<uintptr_t>(row) & 15u) == 0) && c0 + 128 <= p.k) {
+      const int c0 = 32 * WPI * q;
+      if (((reinterpret_cast<uintptr_t>(row) & 15u) == 0) && c0 + 32 * WPI <= p.k) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 4 * WPI; ++j) {
           const uint4 t = __ldg(reinterpret_cast<const uint4*>(row + c0) + j);
           const __half2* h = reinterpret_cast<const __half2*>(&t);
 #pragma unroll
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
           }
         }
       } else {
-        for (int c = c0; c < c0 + 128 && c < p.k; ++c) m = fmaxf(m, fabsf(__half2float(row[c])));
+        for (int c = c0; c < c0 + 32 * WPI && c < p.k; ++c) m = fmaxf(m, fabsf(__half2float(row[c])));
       }
       atomicMax(&s_amax[rl], __float_as_uint(m));
     }
@@ -190,13 +194,13 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
     } else {
       rowp = p.codes + (int64_t)r * p.ld;
     }
-    uint32_t v[32];
-    load_quad<QUANT>(p, rowp, 128 * q, s, kQmax, v);
+    uint32_t v[8 * WPI];
+    load_words<QUANT, WPI>(p, rowp, 32 * WPI * q, s, kQmax, v);
     int sum = 0;
-    uint32_t pw[BITS][4];
+    uint32_t pw[BITS][WPI];
 #pragma unroll
-    for (int wi = 0; wi < 4; ++wi) {
-      const int c0 = 128 * q + 32 * wi;
+    for (int wi = 0; wi < WPI; ++wi) {
+      const int c0 = 32 * (WPI * q + wi);
       uint32_t u[8];
       bool bad = false;
 #pragma unroll
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
       uint32_t o[8];
       to_slot_order(u, o);
       if (p.digits) {
-        uint4* dd = reinterpret_cast<uint4*>(p.digits + ((int64_t)r * p.k_words + 4 * q + wi) * 32);
+        uint4* dd = reinterpret_cast<uint4*>(p.digits + ((int64_t)r * p.k_words + WPI * q + wi) * 32);
         dd[0] = make_uint4(o[0], o[1], o[2], o[3]);
         dd[1] = make_uint4(o[4], o[5], o[6], o[7]);
       }
@@ -240,14 +244,19 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
 #pragma unroll
       for (int i = 0; i < BITS; ++i) pw[i][wi] = w[i];
     }
-    // one 16-byte store per plane: canonical [plane][row][k_words] or tile-major
-    // [plane][row/128][Kpad/256][2][128][4] (quad q = half q & 1 of slab q >> 1)
-    uint32_t* dst = p.tiled ? p.planes + ((int64_t)(r >> 7) * (p.k_words >> 3) + (q >> 1)) * 1024 + (q & 1) * 512 +
-                                  (r & 127) * 4
-                            : p.planes + (int64_t)r * p.k_words + 4 * q;
+    // plane stores: canonical [plane][row][k_words] or tile-major [plane][row/128][Kpad/256][2][128][4]
+    // (word w of row r at slab w >> 3, half (w >> 2) & 1, column w & 3); a quad is one 16-byte store
+    const int w0 = WPI * q;
+    uint32_t* dst = p.tiled ? p.planes + ((int64_t)(r >> 7) * (p.k_words >> 3) + (w0 >> 3)) * 1024 + ((w0 >> 2) & 1) * 512 +
+                                  (r & 127) * 4 + (w0 & 3)
+                            : p.planes + (int64_t)r * p.k_words + w0;
 #pragma unroll
-    for (int i = 0; i < BITS; ++i)
-      *reinterpret_cast<uint4*>(dst + (int64_t)i * p.plane_stride) = make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
+    for (int i = 0; i < BITS; ++i) {
+      if constexpr (WPI == 4)
+        *reinterpret_cast<uint4*>(dst + (int64_t)i * p.plane_stride) = make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
+      else
+        dst[(int64_t)i * p.plane_stride] = pw[i][0];
+    }
     atomicAdd(&s_sum[rl], sum);
   }
   __syncthreads();
@@ -256,32 +265,39 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
   if (!p.digits) pack_release();
 }
 
-// rows per CTA: whole rows (row sums without global atomics); tile-major: 32 rows so a warp's store
-// is 32 consecutive rows of one 16-byte column; canonical: enough rows to give every thread a quad
-static int pack_rows_per_cta(const PackArgs& p) {
-  const int Q = p.k_words / 4;
-  if (p.tiled) return 32;
+// rows per CTA: whole rows (row sums without global atomics); tile-major weights: 32 rows so a warp's
+// store is 32 consecutive rows of one 16-byte column; otherwise enough rows to give every thread an item
+static int pack_rows_per_cta(const PackArgs& p, int wpi) {
+  const int Q = p.k_words / wpi;
+  if (p.tiled && wpi == 4) return 32;
   int R = kPackThreads / (Q > 0 ? Q : 1);
   if (R < 1) R = 1;
   if (R > kPackMaxRows) R = kPackMaxRows;
   return R;
 }
 
-template <bool QUANT>
-static cudaError_t launch_pack_t(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {
-  const int R = pack_rows_per_cta(p);
+template <bool QUANT, int WPI>
+static cudaError_t launch_pack_w(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {
+  const int R = pack_rows_per_cta(p, WPI);
   const dim3 grid((p.rows + R - 1) / R), block(kPackThreads);
   const __half* xh = reinterpret_cast<const __half*>(x);
   switch (bits) {
-    case 1: return launch_pdl(pack_kernel<1, QUANT>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
-    case 2: return launch_pdl(pack_kernel<2, QUANT>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
-    case 3: return launch_pdl(pack_kernel<3, QUANT>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
-    case 4: return launch_pdl(pack_kernel<4, QUANT>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
-    case 5: return launch_pdl(pack_kernel<5, QUANT>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
-    case 6: return launch_pdl(pack_kernel<6, QUANT>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
-    case 7: return launch_pdl(pack_kernel<7, QUANT>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
-    default: return launch_pdl(pack_kernel<8, QUANT>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
+    case 1: return launch_pdl(pack_kernel<1, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
+    case 2: return launch_pdl(pack_kernel<2, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
+    case 3: return launch_pdl(pack_kernel<3, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
+    case 4: return launch_pdl(pack_kernel<4, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
+    case 5: return launch_pdl(pack_kernel<5, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
+    case 6: return launch_pdl(pack_kernel<6, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
+    case 7: return launch_pdl(pack_kernel<7, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
+    default: return launch_pdl(pack_kernel<8, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
   }
+}
+
+// activation packs (a digit view, few rows) take one word per thread; everything else quads
+template <bool QUANT>
+static cudaError_t launch_pack_t(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {
+  if (p.digits && p.rows <= 64) return launch_pack_w<QUANT, 1>(p, x, scale, bits, stream);
+  return launch_pack_w<QUANT, 4>(p, x, scale, bits, stream);
 }
 
 cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream) {

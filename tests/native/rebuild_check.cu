@@ -49,6 +49,19 @@ static int check(int ref_slot[32]) {
     }
     apt::to_slot_order(nat, so);
     for (int r = 0; r < 8; ++r) if (so[r] != o[r]) ++bad;
+    // the top-bit rebuild of 1- and 2-bit operands: same slots, digit * 2^(8-Q)
+    if constexpr (Q == 3 || Q == 4) {
+      uint32_t x16[8];
+      apt::rebuild_x16<Q>(w, x16);
+      for (int r = 0; r < 8; ++r) if (x16[r] != (o[r] << 4)) ++bad;
+    }
+    if constexpr (Q <= 2) {
+      uint32_t hi[8];
+      apt::rebuild_hi<Q>(w, hi);
+      for (int r = 0; r < 8; ++r)
+        for (int b = 0; b < 4; ++b)
+          if (((hi[r] >> (8 * b)) & 0xFF) != (((o[r] >> (8 * b)) & 0xFF) << (8 - Q))) ++bad;
+    }
   }
   return bad;
 }

@@ -166,6 +166,8 @@ def _family_cfgs(m, n, k, wb, ab):
         "skinny": dict(base, kernel=4, bm=16, bn=8, bk=256, split_k=8, stages=1, cta_pair=0, cluster_n=1),
         "tc": dict(base, kernel=2, bm=128, bn=16, bk=128, split_k=2, stages=_tc_stages(wb, 16), cta_pair=0,
                    cluster_n=1),
+        "dec": dict(base, kernel=5, bm=32, bn=8 if m <= 8 else 16, bk=256, stages=4, split_k=3, cta_pair=0,
+                    cluster_n=1),
     }
 
 
@@ -186,7 +188,7 @@ def test_config_invariance_families(wb, ab):
 
 # ----------------------------------------------------------------------------- stream order (PDL)
 
-@pytest.mark.parametrize("family", ["gemv", "skinny", "tc", "auto16"])
+@pytest.mark.parametrize("family", ["gemv", "skinny", "tc", "dec", "auto16"])
 def test_repack_same_buffer_stream_order(family):
     """Stream order under programmatic dependent launch (include/apt.h "General contract"): pack W1
     into a buffer, GEMM, re-pack DIFFERENT codes W2 into the SAME buffer and GEMM immediately on one
@@ -549,3 +551,78 @@ def test_zero_point_epilogue(m, n, k, zeros):
     mag = (np.abs(y * ws[None, :] * as_[:, None]) + np.abs(rw[None, :] * ws[None, :] * az0[:, None]) +
            np.abs(ra[:, None] * as_[:, None] * wz0[None, :]) + np.abs(k * az0[:, None] * wz0[None, :]))
     assert (np.abs(got - ref) <= 1e-3 * mag + 2.0 ** -24).all()
+
+
+# ----------------------------------------------------------------------------- register-fed decode GEMM (M <= 16)
+
+def _dec_cfg(m, n, k, wb, ab, split=1, warps=4):
+    return dict(P.select_config(m, n, k, wb, ab), kernel=5, bm=32, bn=8 if m <= 8 else 16, bk=256,
+                stages=warps, split_k=split, cta_pair=0, cluster_n=1)
+
+
+@pytest.mark.parametrize("m", [1, 3, 8, 9, 16])
+@pytest.mark.parametrize("pw,pa", [(1, 1), (1, 2), (2, 2), (2, 8), (3, 4), (4, 4), (5, 3), (8, 8)])
+@pytest.mark.parametrize("split,warps", [(1, 4), (1, 8), (2, 4), (3, 8), (16, 4)])
+def test_dec_matches_oracle(m, pw, pa, split, warps):
+    """APT_KERNEL_DEC: int32 signed / bipolar bit-exact and fp16 within 1e-3 on ragged shapes (N not a
+    multiple of 8, 32 or 128; K not a multiple of 256; more K splits and warps than 256-element blocks),
+    tile-major and canonical weights, row and column layouts; the split-K tickets are left zero."""
+    for n, k, tiled in ((333, 700, True), (100, 64, False), (41, 1300, True), (256, 4096, False), (300, 4096, True)):
+        a = signed_codes(m, k, pa, seed=170 + m + pa)
+        w = signed_codes(n, k, pw, seed=180 + pw + n)
+        A = P.pack(_dev(a), pa, digits=True)
+        W = P.pack(_dev(w), pw, tiled=tiled)
+        cfg = _dec_cfg(m, n, k, pw, pa, split, warps)
+        ref = O.gemm_signed(a, w)
+        assert np.array_equal(P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64), ref)
+        got = P.gemm(W, A, out_kind="bipolar", layout="col", config=cfg).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got.T, O.gemm_bipolar(a, pa, w, pw))
+        ws = log_uniform_scales(n, -10, -6, seed=15)
+        as_ = log_uniform_scales(m, -6, -2, seed=16)
+        got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_), config=cfg).cpu().numpy()
+        r = O.scale_fp64(ref, ws, as_)
+        assert (np.abs(got.astype(np.float64) - r) <= 1e-3 * np.abs(r) + 2.0 ** -24).all()
+    if split > 1:
+        ws_t = P.default_workspace(DEV, 0)
+        torch.cuda.synchronize()
+        # the split-K tickets (include/apt.h: the first APT_WS_TICKET_BYTES of the workspace) are left zero
+        assert int(ws_t[:16384].count_nonzero().item()) == 0
+
+
+def test_dec_without_digit_view_and_extremes():
+    """The DEC kernel reading the workspace token expansion (no digit view), and all-extreme codes at
+    the largest K its 2^32 unsigned-sum bound allows for 2-bit weights x 8-bit activations."""
+    m, n, k = 5, 200, 4096
+    a = signed_codes(m, k, 4, seed=1)
+    w = signed_codes(n, k, 2, seed=2)
+    A = P.pack(_dev(a), 4)
+    W = P.pack(_dev(w), 2, tiled=True)
+    got = P.gemm(W, A, config=_dec_cfg(m, n, k, 2, 4, 4)).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, O.gemm_signed(a, w))
+    k = 66048  # Kpad * 255 * 255 < 2^32
+    for av, wv in ((-128, -2), (127, 1), (-128, 1)):
+        a = np.full((16, k), av, dtype=np.int8)
+        w = np.full((40, k), wv, dtype=np.int8)
+        A = P.pack(_dev(a), 8, digits=True)
+        W = P.pack(_dev(w), 2, tiled=True)
+        got = P.gemm(W, A, config=_dec_cfg(16, 40, k, 2, 8, 17)).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, np.full((16, 40), k * av * wv, dtype=np.int64))
+
+
+@pytest.mark.parametrize("n,k", LLAMA7B)
+@pytest.mark.parametrize("m", [1, 8, 16])
+@pytest.mark.parametrize("pw,pa", [(1, 2), (2, 2), (3, 4), (4, 4)])
+@pytest.mark.parametrize("split,warps", [(1, 8), (2, 4)])
+def test_dec_llama7b_full(n, k, m, pw, pa, split, warps):
+    """BASELINE configs[1] at full size through APT_KERNEL_DEC, fp16 + a_scale (the bench's call):
+    every element within 1e-3 of the fp64-scaled C oracle."""
+    a = signed_codes(m, k, pa, seed=config_seed(1, pw, pa, salt=11))
+    w = signed_codes(n, k, pw, seed=config_seed(1, pw, pa, salt=11) + 1)
+    ws = log_uniform_scales(n, -10, -6, seed=n + pw + 1)
+    as_ = log_uniform_scales(m, -6, -2, seed=m + pa + 1)
+    A = P.pack(_dev(a), pa, digits=True)
+    W = P.pack(_dev(w), pw, tiled=True)
+    cfg = _dec_cfg(m, n, k, pw, pa, split, warps)
+    got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_), config=cfg).cpu().numpy()
+    ref = O.scale_fp64(c_gemm_i64(a, w), ws, as_)
+    assert (np.abs(got.astype(np.float64) - ref) <= 1e-3 * np.abs(ref) + 2.0 ** -24).all()

@@ -1,6 +1,8 @@
 """Run one APT GEMM configuration a few times (for ncu captures).
 
-  python tools/prof_one.py M N K wbits abits [reps] [bn]
+  python tools/prof_one.py M N K wbits abits [reps] [bn] [key=value,...]
+The optional last argument overrides config fields, e.g. kernel=5,bm=32,split_k=2 (APT_KERNEL_DEC: bn, bk
+and stages are filled in).
 """
 import os
 import sys
@@ -25,6 +27,12 @@ def main():
         cfg["bn"] = bn
         stage = bn * 128 + wb * 128 * 16
         cfg["stages"] = max(2, min(6, ((110 if bn <= 128 else 220) * 1024) // stage))
+    if len(sys.argv) > 8:
+        for kv in sys.argv[8].split(","):
+            key, v = kv.split("=")
+            cfg[key] = int(v)
+        if cfg["kernel"] == 5:
+            cfg.update(bm=32, bn=8 if m <= 8 else 16, bk=256, cta_pair=0, cluster_n=1)
     out = torch.empty((m, n), dtype=torch.float16, device=dev)
     for _ in range(reps):
         P.pack(a, ab, out=A)
