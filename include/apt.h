@@ -224,8 +224,9 @@ typedef struct {
   int32_t kernel, w_digit, a_digit, bm, bn, bk, stages, split_k, cta_pair, cluster_n, mma_kind;
 } apt_config;
 
-/* Host, pure and deterministic (replaces the paper's lookup table + search, §5.2).
- * p = wbits, q = abits as in the north_star's "W_p x A_q".  Rules (measured on B200):
+/* Host, deterministic for a given loaded table (see apt_table_load; the analytic rules below when no
+ * legal table row applies).
+ * p = wbits, q = abits as in the north_star's "W_p x A_q".  Analytic rules (measured on B200):
  *   M <= 2       -> APT_KERNEL_GEMV, 16 warps per CTA if ceil(N/32) <= 148 else 8;
  *   M <= 8, K <= 4096 -> APT_KERNEL_SKINNY, bn 8, 8 warps per CTA if ceil(N/16) <= 296 else 4;
  *   M <= 64      -> APT_KERNEL_TC decode tile (bn 16 for M <= 16 else 64), K split over a cluster so that
@@ -235,6 +236,32 @@ typedef struct {
  *         APT_ERR_UNSUPPORTED (int32 bound, reading Q8). */
 APT_API apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits,
                              apt_config* out /* host */);
+
+/* Autotuned configuration table (the paper's lookup table, Best Kernel Search and
+ * Approximate Matching, §5.2).  Host-only, thread-safe (one mutex-guarded table per process).
+ * File format: text, '#' comments, one row per key:
+ *   M N K wbits abits  kernel w_digit a_digit bm bn bk stages split_k cta_pair cluster_n mma_kind  us
+ * (the apt_config fields in declaration order, then the measured time in microseconds).  tools/tune.py
+ * writes it by timing every config apt_enumerate_configs returns.
+ * apt_select_config consults the table first: the exact key, else the nearest key by
+ *   d = |log2 M - log2 M'| + |log2 N - log2 N'| + |log2 K - log2 K'|
+ * among rows with the same (wbits, abits) (any row if none has them), ties -> smaller measured time, then
+ * smaller key; the row's config is returned only if it is legal for the queried shape, else the analytic
+ * rules decide.  Rows loaded later replace earlier rows with the same key.
+ * apt_table_load: APT_ERR_INVALID_ARGUMENT for a missing file or a malformed row (nothing is loaded then).
+ * apt_table_lookup: the nearest row's stored config and its distance (0 = exact);
+ *   APT_ERR_UNSUPPORTED if the table is empty. */
+APT_API apt_status apt_table_load(const char* path /* host */);
+APT_API void apt_table_clear(void);
+APT_API int32_t apt_table_size(void);
+APT_API apt_status apt_table_lookup(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits,
+                                    apt_config* out /* host */, double* distance /* host, nullable */);
+/* Host.  The search space of the Best Kernel Search: every config legal for (M, N, K, wbits, abits)
+ * (GEMV warps 8/16; SKINNY bn 8/16 x warps 4/8/16; DEC warps 4/8 x split 1,2,3,4,6,8; TC bn 16/64/128/256 x
+ * cluster 1/2/4 x split 1..8), in that order.  Writes up to `cap` of them to `out` (nullable) and returns
+ * how many exist (0 for invalid arguments or the int32 bound). */
+APT_API int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits,
+                                      apt_config* out /* host */, int32_t cap);
 
 /* Host.  Device workspace bytes apt_gemm needs for (cfg, M, N, K).
  * Layout: [APT_WS_TICKET_BYTES of split-K tickets at offset 0 — the same place for every call]

@@ -20,7 +20,8 @@ ABI_VERSION = 4  # include/apt.h APT_ABI_VERSION this binding marshals for
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes", "apt_gemm_zp_workspace_bytes",
-            "apt_gemm", "apt_status_string", "apt_abi_version"]
+            "apt_gemm", "apt_status_string", "apt_abi_version", "apt_table_load", "apt_table_clear", "apt_table_size",
+            "apt_table_lookup", "apt_enumerate_configs"]
 
 
 class AptPacked(ctypes.Structure):
@@ -84,6 +85,16 @@ def lib():
         L.apt_status_string.argtypes = [ctypes.c_int]
         L.apt_abi_version.restype = ctypes.c_int32
         L.apt_abi_version.argtypes = []
+        L.apt_table_load.restype = ctypes.c_int
+        L.apt_table_load.argtypes = [ctypes.c_char_p]
+        L.apt_table_clear.restype = None
+        L.apt_table_clear.argtypes = []
+        L.apt_table_size.restype = ctypes.c_int32
+        L.apt_table_size.argtypes = []
+        L.apt_table_lookup.restype = ctypes.c_int
+        L.apt_table_lookup.argtypes = [ctypes.c_int32] * 5 + [ctypes.POINTER(AptConfig), ctypes.POINTER(ctypes.c_double)]
+        L.apt_enumerate_configs.restype = ctypes.c_int32
+        L.apt_enumerate_configs.argtypes = [ctypes.c_int32] * 5 + [ctypes.POINTER(AptConfig), ctypes.c_int32]
         v = int(L.apt_abi_version())
         if v != ABI_VERSION:
             raise ImportError(f"{LIB_PATH} has ABI version {v}, this binding needs {ABI_VERSION}: rebuild it")

@@ -163,6 +163,56 @@ def default_workspace(device, nbytes: int) -> torch.Tensor:
     return ws
 
 
+# ----------------------------------------------------------------------------- autotuned table (NEXT-3)
+
+TABLE_DIR = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.abspath(__file__)), "tables")
+DEFAULT_TABLE = __import__("os").path.join(TABLE_DIR, "b200.apt")
+
+
+def load_table(path: str) -> int:
+    """apt_table_load: merge an autotuned configuration table (§5.2 P:328-335) into the library's table;
+    apt_select_config consults it before its analytic rules.  Returns the table size."""
+    L.check("apt_table_load", L.lib().apt_table_load(str(path).encode()))
+    return int(L.lib().apt_table_size())
+
+
+def clear_table() -> None:
+    L.lib().apt_table_clear()
+
+
+def table_size() -> int:
+    return int(L.lib().apt_table_size())
+
+
+def table_lookup(M: int, N: int, K: int, wbits: int, abits: int):
+    """(config dict, distance) of the nearest table row (distance 0 = exact key), or None if empty."""
+    c = L.AptConfig()
+    d = ctypes.c_double()
+    rc = L.lib().apt_table_lookup(M, N, K, wbits, abits, ctypes.byref(c), ctypes.byref(d))
+    if rc == L.APT_ERR_UNSUPPORTED:
+        return None
+    L.check("apt_table_lookup", rc)
+    return c.as_dict(), float(d.value)
+
+
+def enumerate_configs(M: int, N: int, K: int, wbits: int, abits: int) -> list:
+    """apt_enumerate_configs: every legal configuration for the problem (the Best Kernel Search space)."""
+    n = int(L.lib().apt_enumerate_configs(M, N, K, wbits, abits, None, 0))
+    arr = (L.AptConfig * max(n, 1))()
+    L.lib().apt_enumerate_configs(M, N, K, wbits, abits, arr, n)
+    return [arr[i].as_dict() for i in range(n)]
+
+
+def load_default_table() -> int:
+    """Load the shipped B200 table (tables/b200.apt, written by tools/tune.py) unless APT_TABLE says
+    otherwise: a path, or "none"."""
+    import os
+    path = os.environ.get("APT_TABLE", DEFAULT_TABLE)
+    if path.lower() == "none" or not os.path.exists(path):
+        return table_size()
+    return load_table(path)
+
+
 def select_config(M: int, N: int, K: int, wbits: int, abits: int) -> dict:
     """apt_select_config (p = wbits, q = abits)."""
     c = L.AptConfig()

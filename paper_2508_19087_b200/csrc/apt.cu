@@ -1,8 +1,12 @@
 // apt.cu — the C-ABI boundary (include/apt.h): argument validation, the config selector and
 // kernel dispatch.  No torch types, no allocation, no synchronization.
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "../../include/apt.h"
@@ -104,6 +108,73 @@ apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_pa
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------------------
+// Autotuned configuration table (the paper's lookup table + Best Kernel Search +
+// Approximate Matching, §5.2).  The table is filled offline by measuring every legal config
+// (apt_enumerate_configs) per problem key (tools/tune.py) and loaded with apt_table_load.  Lookup: the
+// exact key (M, N, K, wbits, abits), else the nearest key by d = |log2 M - log2 M'| + |log2 N - log2 N'| +
+// |log2 K - log2 K'| among entries with the same (wbits, abits) — any (wbits, abits) if none — ties broken
+// by the smaller measured time, then the smaller key.  A found config is used only if it is legal for the
+// queried shape; otherwise the analytic rules decide.
+namespace {
+struct TableEntry {
+  int32_t M, N, K, wbits, abits;
+  apt_config cfg;
+  double us;
+};
+std::mutex g_tab_mu;
+std::vector<TableEntry> g_tab;
+
+double key_dist(const TableEntry& e, int32_t M, int32_t N, int32_t K) {
+  return std::fabs(std::log2((double)M) - std::log2((double)e.M)) + std::fabs(std::log2((double)N) - std::log2((double)e.N)) +
+         std::fabs(std::log2((double)K) - std::log2((double)e.K));
+}
+
+bool key_less(const TableEntry& a, const TableEntry& b) {
+  if (a.M != b.M) return a.M < b.M;
+  if (a.N != b.N) return a.N < b.N;
+  if (a.K != b.K) return a.K < b.K;
+  if (a.wbits != b.wbits) return a.wbits < b.wbits;
+  return a.abits < b.abits;
+}
+
+// nearest entry (see above); false if the table is empty
+bool table_find(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, TableEntry* hit, double* dist) {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (g_tab.empty()) return false;
+  bool same_pq = false;
+  for (const TableEntry& e : g_tab) same_pq |= (e.wbits == wbits && e.abits == abits);
+  const TableEntry* best = nullptr;
+  double bd = 0;
+  for (const TableEntry& e : g_tab) {
+    if (same_pq && (e.wbits != wbits || e.abits != abits)) continue;
+    const double d = key_dist(e, M, N, K) + ((e.wbits == wbits && e.abits == abits) ? 0.0 : 0.0);
+    bool better = !best || d < bd - 1e-12;
+    if (best && std::fabs(d - bd) <= 1e-12) better = e.us < best->us || (e.us == best->us && key_less(e, *best));
+    if (better) { best = &e; bd = d; }
+  }
+  *hit = *best;
+  *dist = bd;
+  return true;
+}
+
+bool table_select(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, apt_config* out) {
+  TableEntry e;
+  double d;
+  if (!table_find(M, N, K, wbits, abits, &e, &d)) return false;
+  apt_config c = e.cfg;
+  c.w_digit = wbits;  // digit widths follow the operand widths (full-width digits)
+  c.a_digit = abits;
+  if (c.kernel == APT_KERNEL_TC) c.stages = apt::tc_stages(wbits, c.bn);
+  if (validate_config(&c, M, N, K, wbits, abits) != APT_OK) return false;
+  *out = c;
+  return true;
+}
+
+apt_status select_analytic(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, apt_config* out);
+}  // namespace
+
+
 extern "C" {
 
 int32_t apt_abi_version(void) { return APT_ABI_VERSION; }
@@ -188,6 +259,15 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
   if (!out || M <= 0 || N <= 0 || K <= 0 || wbits < 1 || wbits > 8 || abits < 1 || abits > 8)
     return APT_ERR_INVALID_ARGUMENT;
   if (!bound_ok(K, wbits, abits)) return APT_ERR_UNSUPPORTED;
+  // the autotuned table first (NEXT-3, §5.2): exact key or nearest key, if legal for the shape
+  if (table_select(M, N, K, wbits, abits, out)) return APT_OK;
+  return select_analytic(M, N, K, wbits, abits, out);
+}
+
+}  // extern "C"
+
+namespace {
+apt_status select_analytic(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, apt_config* out) {
   std::memset(out, 0, sizeof(*out));
   const int kNumSMs = device_sms();
   const int kw = (int)(kpad_of(K) / 32);
@@ -249,6 +329,9 @@ apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int
   out->stages = apt::tc_stages(wbits, out->bn);
   return APT_OK;
 }
+}  // namespace
+
+extern "C" {
 
 // workspace areas (include/apt.h apt_gemm_workspace_bytes), offsets fixed per (cfg, M, N, K):
 // [split-K tickets, APT_WS_TICKETS uint32, the same place for every call][token digit expansion]
@@ -348,6 +431,89 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   return apt::launch_zp_epilogue(z, s) == cudaSuccess ? APT_OK : APT_ERR_CUDA;
 }
 
+
+apt_status apt_table_load(const char* path) {
+  if (!path) return APT_ERR_INVALID_ARGUMENT;
+  FILE* f = std::fopen(path, "r");
+  if (!f) return APT_ERR_INVALID_ARGUMENT;
+  std::vector<TableEntry> rows;
+  char line[512];
+  bool ok = true;
+  while (std::fgets(line, sizeof(line), f)) {
+    const char* q = line;
+    while (*q == ' ' || *q == '\t') ++q;
+    if (*q == '#' || *q == '\n' || *q == '\0') continue;
+    TableEntry e;
+    std::memset(&e, 0, sizeof(e));
+    apt_config& c = e.cfg;
+    const int n = std::sscanf(q, "%d %d %d %d %d %d %d %d %d %d %d %d %d %d %d %d %lf", &e.M, &e.N, &e.K, &e.wbits,
+                              &e.abits, &c.kernel, &c.w_digit, &c.a_digit, &c.bm, &c.bn, &c.bk, &c.stages, &c.split_k,
+                              &c.cta_pair, &c.cluster_n, &c.mma_kind, &e.us);
+    if (n != 17 || e.M <= 0 || e.N <= 0 || e.K <= 0 || e.wbits < 1 || e.wbits > 8 || e.abits < 1 || e.abits > 8) {
+      ok = false;
+      break;
+    }
+    rows.push_back(e);
+  }
+  std::fclose(f);
+  if (!ok) return APT_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  // a later row for the same key replaces an earlier one
+  for (const TableEntry& e : rows) {
+    bool replaced = false;
+    for (TableEntry& o : g_tab)
+      if (o.M == e.M && o.N == e.N && o.K == e.K && o.wbits == e.wbits && o.abits == e.abits) { o = e; replaced = true; }
+    if (!replaced) g_tab.push_back(e);
+  }
+  return APT_OK;
+}
+
+void apt_table_clear(void) {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  g_tab.clear();
+}
+
+int32_t apt_table_size(void) {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  return (int32_t)g_tab.size();
+}
+
+apt_status apt_table_lookup(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, apt_config* out,
+                            double* distance) {
+  if (!out || M <= 0 || N <= 0 || K <= 0 || wbits < 1 || wbits > 8 || abits < 1 || abits > 8)
+    return APT_ERR_INVALID_ARGUMENT;
+  TableEntry e;
+  double d;
+  if (!table_find(M, N, K, wbits, abits, &e, &d)) return APT_ERR_UNSUPPORTED;
+  *out = e.cfg;
+  if (distance) *distance = d;
+  return APT_OK;
+}
+
+int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, apt_config* out,
+                              int32_t cap) {
+  if (M <= 0 || N <= 0 || K <= 0 || wbits < 1 || wbits > 8 || abits < 1 || abits > 8) return 0;
+  if (!bound_ok(K, wbits, abits)) return 0;
+  std::vector<apt_config> v;
+  auto add = [&](int kernel, int bm, int bn, int bk, int stages, int split, int cn) {
+    apt_config c;
+    std::memset(&c, 0, sizeof(c));
+    c.kernel = kernel; c.w_digit = wbits; c.a_digit = abits; c.bm = bm; c.bn = bn; c.bk = bk; c.stages = stages;
+    c.split_k = split; c.cta_pair = 0; c.cluster_n = cn; c.mma_kind = APT_MMA_I8;
+    if (validate_config(&c, M, N, K, wbits, abits) == APT_OK) v.push_back(c);
+  };
+  for (int sp : {8, 16}) add(APT_KERNEL_GEMV, 32, M, 128, 1, sp, 1);
+  for (int bn : {8, 16})
+    for (int w : {4, 8, 16}) add(APT_KERNEL_SKINNY, 16, bn, 256, 1, w, 1);
+  for (int w : {4, 8})
+    for (int sp : {1, 2, 3, 4, 6, 8}) add(APT_KERNEL_DEC, 32, M <= 8 ? 8 : 16, 256, w, sp, 1);
+  for (int bn : {16, 64, 128, 256})
+    for (int cn : {1, 2, 4})
+      for (int sp = 1; sp <= 8; ++sp) add(APT_KERNEL_TC, 128, bn, 128, apt::tc_stages(wbits, bn), sp, cn);
+  const int n = (int)v.size();
+  for (int i = 0; i < n && i < cap && out; ++i) out[i] = v[i];
+  return n;
+}
 }  // extern "C"
 
 namespace {

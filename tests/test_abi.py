@@ -52,10 +52,22 @@ def _select(M, N, K, wb, ab):
     return rc, c
 
 
+@pytest.fixture(params=["analytic", "table"])
+def table_mode(request):
+    """Selector checks with the table cleared (the analytic rules) and with the shipped autotuned table."""
+    import paper_2508_19087_b200 as P
+    P.clear_table()
+    if request.param == "table":
+        P.load_default_table()
+    yield request.param
+    P.clear_table()
+    P.load_default_table()
+
+
 @pytest.mark.parametrize("M", [1, 2, 3, 8, 16, 64, 2048])
 @pytest.mark.parametrize("N,K", [(4096, 4096), (11008, 4096), (4096, 11008), (256, 256), (7, 1)])
 @pytest.mark.parametrize("wb,ab", [(1, 2), (2, 2), (3, 4), (4, 4), (8, 8)])
-def test_selector_legal_and_deterministic(M, N, K, wb, ab):
+def test_selector_legal_and_deterministic(M, N, K, wb, ab, table_mode):
     rc, c = _select(M, N, K, wb, ab)
     assert rc == L.APT_OK
     rc2, c2 = _select(M, N, K, wb, ab)
@@ -67,14 +79,20 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab):
         assert M <= 2 and c.bm == 32 and c.bn == M and c.split_k in (8, 16) and c.stages == 1
         assert c.cluster_n == 1 and c.cta_pair == 0
     elif c.kernel == L.APT_KERNEL_SKINNY:
-        assert 2 < M <= 8 and K <= 4096 and c.bm == 16 and c.bn == 8 and c.bk == 256
-        assert c.split_k in (4, 8) and c.stages == 1 and c.cluster_n == 1 and c.cta_pair == 0
+        assert M <= 16 and c.bm == 16 and c.bn in (8, 16) and c.bk == 256
+        assert c.split_k in (4, 8, 16) and c.stages == 1 and c.cluster_n == 1 and c.cta_pair == 0
+        if table_mode == "analytic":
+            assert 2 < M <= 8 and K <= 4096 and c.bn == 8 and c.split_k in (4, 8)
+    elif c.kernel == L.APT_KERNEL_DEC:
+        assert table_mode == "table" and M <= 16 and c.bm == 32 and c.bn == (8 if M <= 8 else 16) and c.bk == 256
+        assert c.stages in (4, 8) and 1 <= c.split_k <= 32 and c.cluster_n == 1 and c.cta_pair == 0
     else:
         assert c.kernel == L.APT_KERNEL_TC and M > 2
         assert c.bm == 128 and c.bn in (16, 64, 128, 256) and c.cluster_n in (1, 2, 4)
         assert 1 <= c.split_k <= 8 and c.cluster_n * c.split_k <= 8
-        assert c.bn >= min(M, 128 if M > 64 else 64)
         assert c.split_k == 1 or (c.bn <= 64 and c.cluster_n == 1)
+        if table_mode == "analytic":
+            assert c.bn >= min(M, 128 if M > 64 else 64)
 
 
 def test_selector_errors():

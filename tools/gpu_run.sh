@@ -1,7 +1,6 @@
 # GPU session script (edited per call)
 set -x
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/r2_gputest2.txt
-timeout 300 python tools/pack_bench.py > gpurun_out/r2_pack_bench2.jsonl 2>&1
-timeout 600 python bench.py --steps 50 --warmup 5 --no-baselines > gpurun_out/r2_bench2.json 2> gpurun_out/r2_bench2.err
-cat gpurun_out/r2_gputest2.txt; head -14 gpurun_out/r2_pack_bench2.jsonl
+timeout 1500 python tools/tune.py --set decode,prefill --log gpurun_out/r2_tune_log.jsonl > gpurun_out/r2_tune.jsonl 2>&1
+cp paper_2508_19087_b200/tables/b200.apt gpurun_out/b200.apt
+tail -3 gpurun_out/r2_tune.jsonl
