@@ -217,7 +217,13 @@ typedef enum {
  *              once per cluster with TMA multicast (1, 2 or 4)
  *   mma_kind : tensor-core operand kind (apt_mma_kind)                                                  */
 typedef enum {
-  APT_MMA_I8 = 0    /* u8 x u8 -> s32 digits (tcgen05 kind::i8 / mma.sync u8 / dp4a)                  */
+  APT_MMA_I8 = 0,   /* u8 x u8 -> s32 digits (tcgen05 kind::i8 / mma.sync u8 / dp4a)                  */
+  APT_MMA_MXF4 = 1  /* signed codes as e2m1 (fp4) digits, tcgen05 kind::mxf4 with unit UE8M0 block scales,
+                       f32 accumulator (exact: every partial sum is an integer below 2^24), twice the i8
+                       MMA rate.  wbits, abits <= 3 (signed {-4..3} is a subset of e2m1); APT_KERNEL_TC
+                       only, bn 128 / 256, split_k 1, cluster_n 1, Kpad * 16 < 2^24.  Tokens are expanded
+                       from the activation planes into the workspace's expansion area (the digit view is
+                       not used), so the workspace is required (apt_gemm_workspace_bytes).           */
 } apt_mma_kind;
 
 typedef struct {
@@ -258,7 +264,7 @@ APT_API apt_status apt_table_lookup(int32_t M, int32_t N, int32_t K, int32_t wbi
                                     apt_config* out /* host */, double* distance /* host, nullable */);
 /* Host.  The search space of the Best Kernel Search: every config legal for (M, N, K, wbits, abits)
  * (GEMV warps 8/16; SKINNY bn 8/16 x warps 4/8/16; DEC warps 4/8 x split 1,2,3,4,6,8; TC bn 16/64/128/256 x
- * cluster 1/2/4 x split 1..8), in that order.  Writes up to `cap` of them to `out` (nullable) and returns
+ * cluster 1/2/4 x split 1..8; TC kind::mxf4 bn 128/256 when wbits, abits <= 3), in that order.  Writes up to `cap` of them to `out` (nullable) and returns
  * how many exist (0 for invalid arguments or the int32 bound). */
 APT_API int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits,
                                       apt_config* out /* host */, int32_t cap);

@@ -269,8 +269,8 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
         L.check("apt_select_config", L.lib().apt_select_config(M, N, K, W.bits, A.bits, ctypes.byref(cc)))
     fn = L.lib().apt_gemm_zp_workspace_bytes if zp else L.lib().apt_gemm_workspace_bytes
     ws_need = int(fn(ctypes.byref(cc), M, N, K))
-    if A.digits is not None and not zp and cc.kernel != L.APT_KERNEL_DEC:
-        ws_need = 0  # the digit view replaces the token expansion area
+    if A.digits is not None and not zp and cc.kernel != L.APT_KERNEL_DEC and cc.mma_kind != L.APT_MMA_MXF4:
+        ws_need = 0  # the digit view replaces the token expansion area (kind::mxf4 expands e2m1 tokens)
     if ws_need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < ws_need):
         if workspace is not None:
             raise ValueError(f"workspace holds {workspace.numel() * workspace.element_size()} bytes, "

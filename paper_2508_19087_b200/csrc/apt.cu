@@ -63,7 +63,17 @@ apt_status validate_packed(const apt_packed* P, int32_t rows, int32_t k, int32_t
 apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits) {
   const int kw = (int)(kpad_of(K) / 32);
   if (c->w_digit != wbits || c->a_digit != abits) return APT_ERR_UNSUPPORTED;  // full-width digits only
-  if (c->mma_kind != APT_MMA_I8) return APT_ERR_UNSUPPORTED;
+  if (c->mma_kind != APT_MMA_I8 && c->mma_kind != APT_MMA_MXF4) return APT_ERR_UNSUPPORTED;
+  if (c->mma_kind == APT_MMA_MXF4) {
+    // signed e2m1 digits: codes of at most 3 bits; the tcgen05 prefill tile, one K range, no cluster;
+    // f32 accumulation exact while every partial sum is an integer below 2^24 (|x y| <= 16)
+    if (wbits > 3 || abits > 3 || c->kernel != APT_KERNEL_TC) return APT_ERR_UNSUPPORTED;
+    if ((c->bn != 128 && c->bn != 256) || c->split_k != 1 || c->cluster_n != 1 || c->bm != 128 || c->bk != 128)
+      return APT_ERR_UNSUPPORTED;
+    if (c->stages != apt::tc_stages(wbits, c->bn) || c->cta_pair != 0) return APT_ERR_UNSUPPORTED;
+    if (kpad_of(K) * 16ll >= (1ll << 24)) return APT_ERR_UNSUPPORTED;
+    return APT_OK;
+  }
   if (c->kernel == APT_KERNEL_GEMV) {
     if (M > 4 || c->bm != 32 || c->bn != M || c->bk != 128 || (c->split_k != 8 && c->split_k != 16) ||
         c->stages != 1)
@@ -381,7 +391,8 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   st = validate_config(&c, M, N, K, wbits, abits);
   if (st != APT_OK) return st;
   const size_t dec_ws = ws_dec_bytes(&c, N);
-  const size_t need0 = dec_ws ? ws_dec_off(M, K) + dec_ws : (A->digits ? 0 : APT_WS_TICKET_BYTES + ws_expand_bytes(M, K));
+  const bool expand = !A->digits || c.mma_kind == APT_MMA_MXF4;  // the token expansion area is used
+  const size_t need0 = dec_ws ? ws_dec_off(M, K) + dec_ws : (expand ? APT_WS_TICKET_BYTES + ws_expand_bytes(M, K) : 0);
   // zero points (NEXT-2): exact int32 Y into the workspace after the digit-expansion area, then the
   // elementwise zero-point epilogue
   const bool zp = kind == APT_OUT_F16_SCALED && (scales->w_zero || scales->a_zero);
@@ -510,6 +521,13 @@ int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, in
   for (int bn : {16, 64, 128, 256})
     for (int cn : {1, 2, 4})
       for (int sp = 1; sp <= 8; ++sp) add(APT_KERNEL_TC, 128, bn, 128, apt::tc_stages(wbits, bn), sp, cn);
+  for (int bn : {128, 256}) {  // kind::mxf4 (wbits, abits <= 3)
+    apt_config c;
+    std::memset(&c, 0, sizeof(c));
+    c.kernel = APT_KERNEL_TC; c.w_digit = wbits; c.a_digit = abits; c.bm = 128; c.bn = bn; c.bk = 128;
+    c.stages = apt::tc_stages(wbits, bn); c.split_k = 1; c.cluster_n = 1; c.mma_kind = APT_MMA_MXF4;
+    if (validate_config(&c, M, N, K, wbits, abits) == APT_OK) v.push_back(c);
+  }
   const int n = (int)v.size();
   for (int i = 0; i < n && i < cap && out; ++i) out[i] = v[i];
   return n;
@@ -521,6 +539,25 @@ apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_pa
                           int32_t M, int32_t N, int32_t wbits, int32_t abits, void* workspace, cudaStream_t s) {
   // the TC kernel reads the activation operand as kernel-order u8 digits: the packed view, or
   // expanded now into the workspace
+  if (c.mma_kind == APT_MMA_MXF4) {
+    // kind::mxf4: tokens as signed e2m1 nibbles, expanded from the activation planes into the workspace;
+    // the f32 accumulator is already the signed product (no offset-digit correction: h_w = h_a = 0)
+    if (A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
+    uint8_t* xp = reinterpret_cast<uint8_t*>(workspace) + APT_WS_TICKET_BYTES;
+    cudaError_t err = apt::launch_expand_tokens_mx(A->planes, (int64_t)M * A->k_words, M, A->k_words, abits, xp, s);
+    if (err != cudaSuccess) return APT_ERR_CUDA;
+    apt::TcArgs p;
+    p.wp = W->planes;
+    p.w_tiled = W->layout == APT_PACK_TILED ? 1 : 0;
+    p.w_pstride = (int64_t)(p.w_tiled ? (N + 127) / 128 * 128 : N) * W->k_words;
+    p.adig = xp;
+    p.k_words = W->k_words;
+    p.e = e;
+    p.e.h_w = 0;
+    p.e.h_a = 0;
+    err = apt::launch_gemm_tc(p, wbits, c.bn, 1, 1, 1, s);
+    return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+  }
   const uint8_t* adig = A->digits;
   if (!adig && A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
   if (!adig) {
@@ -566,7 +603,7 @@ apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_pa
     p.adig = adig;
     p.k_words = W->k_words;
     p.e = e;
-    cudaError_t err = apt::launch_gemm_tc(p, wbits, c.bn, c.cluster_n, c.split_k, s);
+    cudaError_t err = apt::launch_gemm_tc(p, wbits, c.bn, c.cluster_n, c.split_k, 0, s);
     return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   return APT_ERR_UNSUPPORTED;

@@ -128,6 +128,41 @@ __host__ __device__ __forceinline__ void rebuild_x16(const uint32_t* w, uint32_t
   }
 }
 
+// Signed e2m1 (fp4) digits for the kind::mxf4 tensor-core path (1 <= Q <= 3): the signed code
+// x = u - 2^(Q-1) in [-4, 3] is exactly representable in e2m1 (0, 0.5, 1, 1.5, 2, 3, 4, 6 and signs;
+// nibble = sign << 3 | magnitude code, |x| 1 -> 2, 2 -> 4, 3 -> 5, 4 -> 6).  Each nibble bit is a boolean
+// function of the Q plane bits (one lop3 per bit plane), then the first two butterfly stages of
+// rebuild8 interleave the four bit planes into nibbles: g[c] nibble 2b = element 8b + rev3(2c), nibble
+// 2b + 1 = element 8b + rev3(2c + 1) (rebuild8's slots, two per byte), so weights and tokens rebuilt
+// with this function agree on K.  16 bytes per 32 elements.
+template <int Q>
+__host__ __device__ __forceinline__ void rebuild_e2m1(const uint32_t* w, uint32_t (&g)[4]) {
+  static_assert(Q >= 1 && Q <= 3, "e2m1 holds signed codes of at most 3 bits");
+  uint32_t b0, b1, b2, b3;
+  if constexpr (Q == 1) {  // x = u0 - 1: -1 -> 1010, 0 -> 0000
+    b3 = ~w[0];
+    b2 = 0u;
+    b1 = ~w[0];
+    b0 = 0u;
+  } else if constexpr (Q == 2) {  // x = u - 2: -2 -> 1100, -1 -> 1010, 0 -> 0000, 1 -> 0010
+    b3 = ~w[1];
+    b2 = ~(w[1] | w[0]);
+    b1 = w[0];
+    b0 = 0u;
+  } else {  // x = u - 4: -4 1110, -3 1101, -2 1100, -1 1010, 0 0000, 1 0010, 2 0100, 3 0101
+    const uint32_t u0 = w[0], u1 = w[1], u2 = w[2];
+    b3 = ~u2;
+    b2 = (u2 & u1) | (~u2 & ~(u1 & u0));
+    b1 = (u2 & ~u1 & u0) | (~u2 & ~(u1 ^ u0));
+    b0 = u0 & ~(u2 ^ u1);
+  }
+  uint32_t e01, f01, e23, f23;
+  bf_pair(b0, b1, 1, 0x55555555u, e01, f01);
+  bf_pair(b2, b3, 1, 0x55555555u, e23, f23);
+  bf_pair(e01, e23, 2, 0x33333333u, g[0], g[1]);
+  bf_pair(f01, f23, 2, 0x33333333u, g[2], g[3]);
+}
+
 // The inverse of rebuild8<Q> (the pack direction): 8 registers of digits in rebuild8's slot order
 // -> Q plane words (element c -> bit c).  bf_pair is an involution for a fixed (s, m), so the
 // inverse is the same butterfly run backwards.  Digits must be < 2^Q.

@@ -83,6 +83,17 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
+// kind::mxf4 block-scaled MMA (M=128, N, K=64 e2m1 x e2m1 -> f32), A from TMEM, unit UE8M0 scale factors
+// in TMEM (sfa / sfb columns hold 0x7F = 2^0 in every byte)
+__device__ __forceinline__ void tc_mma_mxf4(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc,
+                                            uint32_t sfa, uint32_t sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb)
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -156,6 +167,32 @@ cudaError_t launch_expand_tokens(const uint32_t* ap, int64_t a_pstride, int M, i
                     ap, a_pstride, M, k_words, abits, out);
 }
 
+// Activation planes [abits][M][k_words] -> signed e2m1 nibbles [M][Kpad / 2] (rebuild_e2m1 order, 16
+// bytes per 32-element word): the token operand of the kind::mxf4 path (abits <= 3).
+__global__ void __launch_bounds__(256) expand_tokens_mx_kernel(const uint32_t* __restrict__ ap, int64_t a_pstride,
+                                                               int32_t M, int32_t k_words, int32_t abits,
+                                                               uint8_t* __restrict__ ws) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)M * k_words) return;
+  uint32_t w[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) w[i] = i < abits ? __ldg(ap + (int64_t)i * a_pstride + idx) : 0u;
+  uint32_t g[4];
+  if (abits == 1) rebuild_e2m1<1>(w, g);
+  else if (abits == 2) rebuild_e2m1<2>(w, g);
+  else rebuild_e2m1<3>(w, g);
+  *reinterpret_cast<uint4*>(ws + idx * 16) = make_uint4(g[0], g[1], g[2], g[3]);
+}
+
+cudaError_t launch_expand_tokens_mx(const uint32_t* ap, int64_t a_pstride, int M, int k_words, int abits, uint8_t* out,
+                                    cudaStream_t stream) {
+  const int64_t total = (int64_t)M * k_words;
+  return launch_pdl(expand_tokens_mx_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, stream, dim3(1, 1, 1),
+                    ap, a_pstride, M, k_words, abits, out);
+}
+
 // ------------------------------------------------------------------------------------ main kernel
 template <int WB, int BN, int STAGES>
 struct TcSmem {
@@ -225,9 +262,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // token rows and multicasts them to all CN, so the token tile crosses L2 -> SM once per cluster.
 // gridDim.z = S > 1 (with CN = 1): the K steps are split over a (1, 1, S) cluster and the S partial
 // accumulator tiles are reduced through distributed shared memory (decode-sized token counts).
-template <int WB, int BN, int STAGES, int CN>
+// MX: the kind::mxf4 variant (wbits, abits <= 3; S == 1, BN >= 128): one MMA step = one weight chunk
+// = 256 K elements (both 2 KB halves of a tile-major slab), weights rebuilt as signed e2m1 nibbles
+// (rebuild_e2m1) into the same 32 TMEM columns per step, tokens as the e2m1 view (128 bytes per row and
+// step), 4 x tcgen05.mma kind::mxf4 (K = 64) per step into an f32 accumulator that holds the exact
+// signed product (every partial sum is an integer below 2^24; reading R-MX).
+template <int WB, int BN, int STAGES, int CN, bool MX>
 __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w,
                                                          const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
+  static_assert(!MX || (WB <= 3 && BN >= 128), "kind::mxf4 path: wbits <= 3, token tiles of 128 / 256");
   using L = TcSmem<WB, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
 #ifdef APT_TC_GTRACE
@@ -256,8 +299,10 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
   // (summed in the epilogue), so consecutive MMAs carry no accumulator dependency and pipeline in the
   // tensor core instead of serialising on the MMA latency
   constexpr int kNAcc = BN == 16 ? APT_DEC_NACC : 1;
-  constexpr uint32_t kTmemCols = (BN * kNAcc + 32 * L::kAStages) <= 256 ? 256 : 512;
+  constexpr uint32_t kSfCols = MX ? 32 : 0;  // unit scale factors (mxf4): 16 columns for A, 16 for B
+  constexpr uint32_t kTmemCols = (BN * kNAcc + 32 * L::kAStages + kSfCols) <= 256 ? 256 : 512;
   constexpr uint32_t kAcol0 = BN * kNAcc;  // A ring after the accumulator columns
+  constexpr uint32_t kScol0 = kAcol0 + 32 * L::kAStages;
   constexpr int kRowsPerCta = BN / CN;
   constexpr uint16_t kMask = (uint16_t)((1u << CN) - 1);
 
@@ -273,6 +318,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
   const int kb = (int)(((int64_t)blockIdx.z * nk) / S);
   const int ke = (int)(((int64_t)(blockIdx.z + 1) * nk) / S);
   const int nloc = ke - kb;
+  const int nms = MX ? nloc / 2 : nloc;  // MMA steps (mxf4: 256 K elements = one weight chunk each)
   pdl_launch_dependents();
   if (threadIdx.x == 0) { TRACE(6, 0); GTRACE(0); GTRACE(7); }
 
@@ -349,7 +395,7 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
     }
     for (int c = 0; c < L::kWSlots; ++c) {
       mbar_init(wfull(c), 1);
-      mbar_init(wempty(c), 8);      // the 8 converter warps (each reads one K step of the chunk)
+      mbar_init(wempty(c), MX ? 4 : 8);  // the converter warps reading the chunk (one step each; mxf4: one parity)
     }
     for (int a = 0; a < L::kAStages; ++a) {
       mbar_init(a_full(a), 4);
@@ -411,7 +457,16 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
         for (int j = 0; j < nloc; ++j) tma_load_2d(sB + j * L::kBBytes, &tm_b, full(0), (kb + j) * kTcBK, m0);
         if (kTokEarly && tiled) issue_pre(2);
       }
-      for (int j = 0; j < nloc; ++j) {
+      if constexpr (MX) {
+        for (int j = 0; j < nms; ++j) {
+          if (j >= n_pre) issue_w(j);  // weight chunk j = MMA step j
+          const int s = j % STAGES;
+          mbar_wait(empty(s), ((j / STAGES) & 1) ^ 1);
+          mbar_expect_tx(full(s), L::kBBytes);
+          tma_load_2d(sB + s * L::kBBytes, &tm_b, full(s), (kb / 2 + j) * 128, m0);  // 128 bytes = 256 K
+        }
+      }
+      for (int j = 0; j < (MX ? 0 : nloc); ++j) {
         const int ks = kb + j;
         if (j % 2 == 0 && j / 2 >= n_pre) {  // next weight chunk
           issue_w(j / 2);
@@ -433,10 +488,14 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = (2u << 4)                       // D = s32
-                                 | ((uint32_t)(BN >> 3) << 17)   // N
-                                 | ((uint32_t)(kTcBM >> 4) << 24);  // M ; A, B = u8, K-major
-      for (int j = 0; j < nloc; ++j) {
+      constexpr uint32_t idesc = MX ? ((1u << 7) | (1u << 10)              // A, B = e2m1
+                                        | ((uint32_t)(BN >> 3) << 17)     // N
+                                        | (1u << 23)                      // scale factors UE8M0
+                                        | ((uint32_t)(kTcBM >> 4) << 24))  // M ; K-major
+                                     : ((2u << 4)                         // D = s32
+                                        | ((uint32_t)(BN >> 3) << 17)     // N
+                                        | ((uint32_t)(kTcBM >> 4) << 24));  // M ; A, B = u8, K-major
+      for (int j = 0; j < nms; ++j) {
         const int s = L::kBAll ? j : j % STAGES;
         const uint32_t ph = (j / STAGES) & 1;
         const int a = j % L::kAStages;
@@ -449,10 +508,14 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
         tc_fence_after();
         const uint64_t bdesc = umma_desc_sw128(sB + s * L::kBBytes);
 #pragma unroll
-        for (int kk = 0; kk < kTcBK / 32; ++kk) {
-          // advance 32 K bytes inside the 128-byte swizzle atom: +2 in the (addr >> 4) field
-          tc_mma_i8(tmem + (uint32_t)((kk % kNAcc) * BN), tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk),
-                    idesc, (kNAcc > 1 ? (j | (kk / kNAcc)) : (j | kk)) != 0);
+        for (int kk = 0; kk < 4; ++kk) {
+          // advance 32 bytes (32 u8 / 64 e2m1) inside the 128-byte swizzle atom: +2 in the (addr >> 4) field
+          if constexpr (MX)
+            tc_mma_mxf4(tmem, tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk), idesc, (j | kk) != 0,
+                        tmem + kScol0, tmem + kScol0 + 16);
+          else
+            tc_mma_i8(tmem + (uint32_t)((kk % kNAcc) * BN), tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk),
+                      idesc, (kNAcc > 1 ? (j | (kk / kNAcc)) : (j | kk)) != 0);
         }
         if (!L::kBAll) {
           if (CN > 1) tc_commit_mc(empty(s), kMask); else tc_commit(empty(s));
@@ -485,31 +548,62 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
 #ifdef APT_CONV_PIPE
     int pend_a = -1;  // A stage whose tcgen05.st is still in flight
 #endif
-    for (int j = par; j < nloc; j += 2) {
-      const int c = j / L::kKpc, q = j % L::kKpc;  // kKpc == 2: each parity reads one step per chunk
+    if constexpr (MX) {
+      // unit UE8M0 scale factors (2^0) for every row / column the MMAs read: parity 0 of each
+      // sub-partition fills its 32 lanes of the 32 scale columns before its first a_full arrive
+      if (par == 0) {
+        uint32_t one[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) one[i] = 0x7F7F7F7Fu;
+        tmem_st32<32>(tmem + lane_off + kScol0, one);
+      }
+    }
+    for (int j = par; j < nms; j += 2) {
+      const int c = MX ? j : j / L::kKpc, q = MX ? 0 : j % L::kKpc;  // kKpc == 2: each parity reads one step per chunk
       if (tiled && c < n_pre) mbar_wait(2 * c < pre_s0 ? wbig0 : wbig, 0);
       else mbar_wait(wfull(c % L::kWSlots), ((c / L::kWSlots) - (tiled ? 1 : 0)) & 1);
       if (lane == 0 && (cw & 3) == 0) TRACE(3, j);
       if (lane == 0 && cw == 0 && j == 0) GTRACE(2);
-      uint4 v[WB];
+      constexpr int kH = MX ? 2 : 1;  // 16-byte pieces per plane and row (mxf4 steps read both halves)
+      uint4 v[kH][WB];
       const uint8_t* wsm = gbase + L::kWOff;
 #pragma unroll
-      for (int i = 0; i < WB; ++i) {
-        const int off = tiled ? (i * L::kWSlots + c % L::kWSlots) * 4096 : (c % L::kWSlots) * L::kWBytes + i * 4096;
-        // tile-major: [q][row][4 words] (lanes read consecutive 16 B); canonical TMA box: [row][8 words]
-        v[i] = *reinterpret_cast<const uint4*>(wsm + off + (p.w_tiled ? q * 2048 + r * 16 : (r * L::kCW + 4 * q) * 4));
-      }
+      for (int h = 0; h < kH; ++h)
+#pragma unroll
+        for (int i = 0; i < WB; ++i) {
+          const int off = tiled ? (i * L::kWSlots + c % L::kWSlots) * 4096 : (c % L::kWSlots) * L::kWBytes + i * 4096;
+          // tile-major: [q][row][4 words] (lanes read consecutive 16 B); canonical TMA box: [row][8 words]
+          const int qq = MX ? h : q;
+          v[h][i] = *reinterpret_cast<const uint4*>(wsm + off + (p.w_tiled ? qq * 2048 + r * 16 : (r * L::kCW + 4 * qq) * 4));
+        }
       __syncwarp();
       if (lane == 0) mbar_arrive(wempty(c % L::kWSlots));
       uint32_t d[32];
+      if constexpr (MX) {
+        // 8 words x 16 bytes of signed e2m1 nibbles (word wi -> TMEM columns 4 wi .. 4 wi + 3)
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        uint32_t w[WB], o[8];
+        for (int wi = 0; wi < 8; ++wi) {
+          uint32_t w[3] = {0u, 0u, 0u}, g[4];
 #pragma unroll
-        for (int i = 0; i < WB; ++i) w[i] = jj == 0 ? v[i].x : jj == 1 ? v[i].y : jj == 2 ? v[i].z : v[i].w;
-        rebuild8<WB>(w, o);
+          for (int i = 0; i < WB; ++i) {
+            const uint4& t = v[wi >> 2][i];
+            const int jj = wi & 3;
+            w[i] = jj == 0 ? t.x : jj == 1 ? t.y : jj == 2 ? t.z : t.w;
+          }
+          if constexpr (MX) rebuild_e2m1<(WB <= 3 ? WB : 3)>(w, g);
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc) d[8 * jj + cc] = o[cc];
+          for (int cc = 0; cc < 4; ++cc) d[4 * wi + cc] = g[cc];
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          uint32_t w[WB], o[8];
+#pragma unroll
+          for (int i = 0; i < WB; ++i) w[i] = jj == 0 ? v[0][i].x : jj == 1 ? v[0][i].y : jj == 2 ? v[0][i].z : v[0][i].w;
+          rebuild8<WB>(w, o);
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) d[8 * jj + cc] = o[cc];
+        }
       }
       const int a = j % L::kAStages;
       const uint32_t pa = (j / L::kAStages) & 1;
@@ -571,6 +665,10 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
       for (int c0 = par * kHalf; c0 < (par + 1) * kHalf; c0 += kChunk) {
         uint32_t acc[kChunk];
         load_acc(c0, acc);
+        if constexpr (MX) {  // f32 accumulator holding an exact integer -> the signed product
+#pragma unroll
+          for (int jj = 0; jj < kChunk; ++jj) acc[jj] = (uint32_t)__float2int_rn(__uint_as_float(acc[jj]));
+        }
         if (n < p.e.N) {
 #pragma unroll
           for (int jj = 0; jj < kChunk; ++jj) {
@@ -699,15 +797,15 @@ int tc_stages(int wbits, int bn) { return tc_stages_ct(wbits, bn); }
 
 size_t tc_workspace_bytes(int M, int k_words) { return (size_t)M * (size_t)k_words * 32u; }
 
-template <int WB, int BN, int ST, int CN>
+template <int WB, int BN, int ST, int CN, bool MX = false>
 static cudaError_t launch_tc4(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int split,
                               cudaStream_t stream) {
   using L = TcSmem<WB, BN, ST>;
   static_assert(L::kTotal <= 227 * 1024, "shared memory budget");
   // the decode tiles are sized for two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
   static_assert(BN != 16 || 2 * (L::kTotal + 1024) <= 228 * 1024, "two CTAs per SM");
-  auto kern = gemm_tc_kernel<WB, BN, ST, CN>;
-  cudaError_t err = set_smem_once<gemm_tc_kernel<WB, BN, ST, CN>>(L::kTotal);
+  auto kern = gemm_tc_kernel<WB, BN, ST, CN, MX>;
+  cudaError_t err = set_smem_once<gemm_tc_kernel<WB, BN, ST, CN, MX>>(L::kTotal);
   if (err != cudaSuccess) return err;
   const int gx = ((p.e.N + kTcBM - 1) / kTcBM + CN - 1) / CN * CN;
   return launch_pdl(kern, dim3(gx, (p.e.M + BN - 1) / BN, split), dim3(384), L::kTotal, stream, dim3(CN, 1, split),
@@ -740,14 +838,15 @@ static cudaError_t launch_tc1(const CUtensorMap& tw, const CUtensorMap& tb, cons
   }
 }
 
-cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, int split, cudaStream_t stream) {
+cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, int split, int mx, cudaStream_t stream) {
   PFN_encodeTiled_t enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tw, tb;
   const int cw = 8;
   if (!make_plane_map(&tw, p.wp, p.k_words, p.e.N, wbits, cw, kTcBM)) return cudaErrorInvalidValue;
   {
-    const cuuint64_t kp = (cuuint64_t)p.k_words * 32;
+    // token view: u8 digits [M][Kpad] (i8), or e2m1 nibbles [M][Kpad / 2] (mxf4); 128-byte boxes
+    const cuuint64_t kp = (cuuint64_t)p.k_words * (mx ? 16 : 32);
     cuuint64_t dims[2] = {kp, (cuuint64_t)p.e.M};
     cuuint64_t strides[1] = {kp};
     cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)(bn / cluster_n)};
@@ -756,6 +855,17 @@ cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, in
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  if (mx) {  // kind::mxf4: wbits <= 3, S = 1, CN = 1, BN 128 / 256 (validated by the caller)
+    switch (wbits * 1000 + bn) {
+      case 1128: return launch_tc4<1, 128, tc_stages_ct(1, 128), 1, true>(tw, tb, p, 1, stream);
+      case 1256: return launch_tc4<1, 256, tc_stages_ct(1, 256), 1, true>(tw, tb, p, 1, stream);
+      case 2128: return launch_tc4<2, 128, tc_stages_ct(2, 128), 1, true>(tw, tb, p, 1, stream);
+      case 2256: return launch_tc4<2, 256, tc_stages_ct(2, 256), 1, true>(tw, tb, p, 1, stream);
+      case 3128: return launch_tc4<3, 128, tc_stages_ct(3, 128), 1, true>(tw, tb, p, 1, stream);
+      case 3256: return launch_tc4<3, 256, tc_stages_ct(3, 256), 1, true>(tw, tb, p, 1, stream);
+      default: return cudaErrorInvalidValue;
+    }
   }
   switch (wbits) {
     case 1: return launch_tc1<1>(tw, tb, p, bn, cluster_n, split, stream);

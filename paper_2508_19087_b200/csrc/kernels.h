@@ -38,7 +38,10 @@ struct TcArgs {
   int32_t k_words;
   EpilogueArgs e;
 };
-cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, int split, cudaStream_t stream);
+cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, int split, int mx, cudaStream_t stream);
+// activation planes -> signed e2m1 token view [M][Kpad / 2] for the kind::mxf4 path (abits <= 3)
+cudaError_t launch_expand_tokens_mx(const uint32_t* ap, int64_t a_pstride, int M, int k_words, int abits, uint8_t* out,
+                                    cudaStream_t stream);
 int tc_stages(int wbits, int bn);
 size_t tc_workspace_bytes(int M, int k_words);
 }  // namespace apt

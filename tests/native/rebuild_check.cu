@@ -55,6 +55,22 @@ static int check(int ref_slot[32]) {
       apt::rebuild_x16<Q>(w, x16);
       for (int r = 0; r < 8; ++r) if (x16[r] != (o[r] << 4)) ++bad;
     }
+    if constexpr (Q <= 3) {
+      // e2m1 digits: the nibble at each element's slot decodes to the signed code u - 2^(Q-1)
+      static const float kE2m1[8] = {0.f, 0.5f, 1.f, 1.5f, 2.f, 3.f, 4.f, 6.f};
+      uint32_t g4[4];
+      apt::rebuild_e2m1<Q>(w, g4);
+      for (int e = 0; e < 32; ++e) {
+        int u = 0;
+        for (int i = 0; i < Q; ++i) u |= (int)((w[i] >> e) & 1u) << i;
+        const int x = u - (1 << (Q - 1));
+        const int s = ref_slot[e];  // rebuild8 slot 4 * reg + byte; reg = 2c + hi, nibble = 2 * byte + hi
+        const int reg = s / 4, byte = s % 4, c = reg / 2, hi = reg % 2;
+        const uint32_t nib = (g4[c] >> (4 * (2 * byte + hi))) & 0xFu;
+        const float v = (nib & 8u ? -1.f : 1.f) * kE2m1[nib & 7u];
+        if (v != (float)x) ++bad;
+      }
+    }
     if constexpr (Q <= 2) {
       uint32_t hi[8];
       apt::rebuild_hi<Q>(w, hi);

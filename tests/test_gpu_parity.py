@@ -626,3 +626,71 @@ def test_dec_llama7b_full(n, k, m, pw, pa, split, warps):
     got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_), config=cfg).cpu().numpy()
     ref = O.scale_fp64(c_gemm_i64(a, w), ws, as_)
     assert (np.abs(got.astype(np.float64) - ref) <= 1e-3 * np.abs(ref) + 2.0 ** -24).all()
+
+
+# ----------------------------------------------------------------------------- kind::mxf4 path (p_w, p_a <= 3)
+
+def _mx_cfg(m, n, k, wb, ab, bn=256):
+    return dict(P.select_config(m, n, k, wb, ab), kernel=2, bm=128, bn=bn, bk=128, stages=_tc_stages(wb, bn), split_k=1,
+                cta_pair=0, cluster_n=1, mma_kind=1)
+
+
+@pytest.mark.parametrize("k", [4096, 28672])
+def test_mxf4_exactness_torture(k):
+    """the f32 accumulation of the e2m1 products must be exact.  All-extreme
+    products (|x y| = 16 and 9) over K = 28,672 (|sum| = 458,752 < 2^24), a large running sum followed by
+    +-1 terms that an accumulator truncating low bits would drop, and alternating signs within every
+    64-element MMA K block — bit-exact against the int64 oracle."""
+    m, n = 256, 256
+    rng = np.random.default_rng(k)
+    a = np.empty((m, k), dtype=np.int8)
+    w = np.empty((n, k), dtype=np.int8)
+    a[:64], w[:64] = -4, -4                                   # +16 everywhere
+    a[64:128], w[64:128] = 3, 3                               # +9 / cross terms -12
+    half = k // 2
+    a[128:192, :half], a[128:192, half:] = -4, rng.choice([-1, 1], size=(64, k - half))
+    w[128:192, :half], w[128:192, half:] = -4, 1             # big sum, then +-1 tail
+    a[192:] = np.where(np.arange(k) % 2 == 0, -4, 1)[None, :]  # alternating 16 / small within each block
+    w[192:] = rng.integers(-4, 4, size=(n - 192, k))
+    A = P.pack(_dev(a), 3)
+    W = P.pack(_dev(w), 3, tiled=True)
+    ref = c_gemm_i64(a, w)
+    for bn in (128, 256):
+        got = P.gemm(W, A, config=_mx_cfg(m, n, k, 3, 3, bn)).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, ref), bn
+
+
+@pytest.mark.parametrize("pw,pa", [(p, q) for p in (1, 2, 3) for q in (1, 2, 3)])
+@pytest.mark.parametrize("bn,tiled", [(128, True), (256, True), (256, False)])
+def test_mxf4_matches_oracle(pw, pa, bn, tiled):
+    """kind::mxf4 on ragged shapes (M, N not multiples of the tile, K not a multiple of 256): int32 signed
+    and bipolar bit-exact, fp16 within 1e-3, row and column layouts, tile-major and canonical weights."""
+    for m, n, k in ((300, 333, 700), (17, 129, 256), (513, 200, 1500)):
+        a = signed_codes(m, k, pa, seed=210 + pa + m)
+        w = signed_codes(n, k, pw, seed=220 + pw + n)
+        A = P.pack(_dev(a), pa, digits=True)
+        W = P.pack(_dev(w), pw, tiled=tiled)
+        cfg = _mx_cfg(m, n, k, pw, pa, bn)
+        ref = O.gemm_signed(a, w)
+        assert np.array_equal(P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64), ref)
+        got = P.gemm(W, A, out_kind="bipolar", layout="col", config=cfg).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got.T, O.gemm_bipolar(a, pa, w, pw))
+        ws = log_uniform_scales(n, -10, -6, seed=25)
+        as_ = log_uniform_scales(m, -6, -2, seed=26)
+        got = P.gemm(W, A, out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_), config=cfg).cpu().numpy()
+        r = O.scale_fp64(ref, ws, as_)
+        assert (np.abs(got.astype(np.float64) - r) <= 1e-3 * np.abs(r) + 2.0 ** -24).all()
+
+
+@pytest.mark.parametrize("pw", [1, 2, 3])
+def test_mxf4_sweep_4096_cube_full(pw):
+    """BASELINE configs[4] at full size through kind::mxf4 for every (p_w, p_a) <= 3: EVERY output
+    element vs the oracle (gemm_signed_blas, exact)."""
+    n = m = k = 4096
+    w = signed_codes(n, k, pw, seed=config_seed(4, pw, 0, salt=9))
+    W = P.pack(_dev(w), pw, tiled=True)
+    for pa in (1, 2, 3):
+        a = signed_codes(m, k, pa, seed=config_seed(4, pw, pa, salt=9))
+        A = P.pack(_dev(a), pa)
+        got = P.gemm(W, A, config=_mx_cfg(m, n, k, pw, pa)).cpu().numpy()
+        assert np.array_equal(got.astype(np.int64), O.gemm_signed_blas(a, w)), pa

@@ -31,6 +31,11 @@ def main():
         for kv in sys.argv[8].split(","):
             key, v = kv.split("=")
             cfg[key] = int(v)
+        if cfg["kernel"] == 2:  # tcgen05: the stage count follows (wbits, bn)
+            match = [c for c in P.enumerate_configs(m, n, k, wb, ab)
+                     if all(c[x] == cfg[x] for x in ("kernel", "bn", "split_k", "cluster_n", "mma_kind"))]
+            if match:
+                cfg = match[0]
         if cfg["kernel"] == 5:
             cfg.update(bm=32, bn=8 if m <= 8 else 16, bk=256, cta_pair=0, cluster_n=1)
     out = torch.empty((m, n), dtype=torch.float16, device=dev)
