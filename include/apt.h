@@ -251,7 +251,8 @@ APT_API apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wb
  * writes it by timing every config apt_enumerate_configs returns.
  * apt_select_config consults the table first: the exact key, else the nearest key by
  *   d = |log2 M - log2 M'| + |log2 N - log2 N'| + |log2 K - log2 K'|
- * among rows with the same (wbits, abits) (any row if none has them), ties -> smaller measured time, then
+ * among rows of the same token regime (M <= 16, M <= 64, M > 64) with the same (wbits, abits) (any row of
+ * that regime if none has them; no match if the regime has no row), ties -> smaller measured time, then
  * smaller key; the row's config is returned only if it is legal for the queried shape, else the analytic
  * rules decide.  Rows loaded later replace earlier rows with the same key.
  * apt_table_load: APT_ERR_INVALID_ARGUMENT for a missing file or a malformed row (nothing is loaded then).

@@ -148,15 +148,24 @@ bool key_less(const TableEntry& a, const TableEntry& b) {
   return a.abits < b.abits;
 }
 
-// nearest entry (see above); false if the table is empty
+// token-count regime of a key: decode (M <= 16), small batch (M <= 64), prefill; rows of another regime
+// are never matched (their kernels answer a different bound: HBM vs tensor)
+int m_class(int32_t M) { return M <= 16 ? 0 : M <= 64 ? 1 : 2; }
+
+// nearest entry (see above); false if no row of the query's M regime exists
 bool table_find(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, TableEntry* hit, double* dist) {
   std::lock_guard<std::mutex> lk(g_tab_mu);
-  if (g_tab.empty()) return false;
-  bool same_pq = false;
-  for (const TableEntry& e : g_tab) same_pq |= (e.wbits == wbits && e.abits == abits);
+  bool any = false, same_pq = false;
+  for (const TableEntry& e : g_tab) {
+    if (m_class(e.M) != m_class(M)) continue;
+    any = true;
+    same_pq |= (e.wbits == wbits && e.abits == abits);
+  }
+  if (!any) return false;
   const TableEntry* best = nullptr;
   double bd = 0;
   for (const TableEntry& e : g_tab) {
+    if (m_class(e.M) != m_class(M)) continue;
     if (same_pq && (e.wbits != wbits || e.abits != abits)) continue;
     const double d = key_dist(e, M, N, K) + ((e.wbits == wbits && e.abits == abits) ? 0.0 : 0.0);
     bool better = !best || d < bd - 1e-12;

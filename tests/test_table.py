@@ -73,12 +73,19 @@ def test_later_rows_replace_and_bad_files(empty_table, tmp_path):
     assert P.table_size() == 1
 
 
-def test_illegal_row_falls_back_to_analytic(empty_table, tmp_path):
-    """A DEC row (M <= 16 only) matched for an M = 2048 query is illegal there: the analytic rules decide."""
+def test_regimes_and_illegal_rows_fall_back_to_analytic(empty_table, tmp_path):
+    """Rows of another token regime (decode M <= 16 vs prefill) never match; a matched row that is illegal
+    for the queried shape (a DEC row for M = 9..16 asked at M = 12 with bn 8 -> illegal) falls back to the
+    analytic rules."""
     analytic = P.select_config(2048, 4096, 4096, 4, 4)
     P.load_table(_write(tmp_path, [_row(16, 4096, 4096, 4, 4, _dec(16, 4, 4), 5.0)]))
-    assert P.table_lookup(2048, 4096, 4096, 4, 4)[0]["kernel"] == 5
+    assert P.table_lookup(2048, 4096, 4096, 4, 4) is None
     assert P.select_config(2048, 4096, 4096, 4, 4) == analytic
+    P.clear_table()
+    analytic = P.select_config(12, 4096, 4096, 4, 4)
+    P.load_table(_write(tmp_path, [_row(8, 4096, 4096, 4, 4, _dec(8, 4, 4), 5.0)]))
+    assert P.table_lookup(12, 4096, 4096, 4, 4)[0]["bn"] == 8
+    assert P.select_config(12, 4096, 4096, 4, 4) == analytic
 
 
 def test_empty_table_lookup(empty_table):
