@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="apt", choices=["apt", "reference"])
     ap.add_argument("--no-baselines", action="store_true", help="skip cuBLAS / oracle / e2e legs")
+    ap.add_argument("--legs", default="all",
+                    help="extra BASELINE configs timed in the same run: all | none | comma list of prefill,llama70b,sweep")
     return ap.parse_args()
 
 
@@ -65,8 +67,9 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-KERNEL_NAMES = {1: "gemm_mma_kernel (mma.sync)", 2: "gemm_tc_kernel (tcgen05)", 3: "gemv_kernel (SIMT dp4a)",
-                4: "gemm_skinny_kernel (mma.sync from registers)"}
+KERNEL_NAMES = {2: "gemm_tc_kernel (tcgen05)", 3: "gemv_kernel (SIMT dp4a)",
+                4: "gemm_skinny_kernel (mma.sync from registers)",
+                5: "gemm_dec_kernel (mma.sync, weights as the streamed B operand)"}
 
 
 def kernel_mix(cfgs):
@@ -375,6 +378,11 @@ def main():
             "per_precision": per_prec, "per_m": per_m, "per_kernel": per_kernel,
             "weight_pack": {"ms": round(wpack_ms, 3), "GB/s": round(wpack_bytes / (wpack_ms * 1e-3) / 1e9, 1)}}
 
+    legs = {"prefill", "llama70b", "sweep"} if args.legs == "all" else set() if args.legs == "none" else \
+        set(args.legs.split(","))
+    if legs:
+        log(f"legs {sorted(legs)}")
+        line.update(run_legs(args, torch, P, dev, stream, world, rank, barrier, legs))
     log("baselines")
     if not args.no_baselines:
         line.update(baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout,
@@ -387,6 +395,188 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+# ----------------------------------------------------------------------------- BASELINE configs[2]-[4] legs
+
+def _chain_us(torch, stream, fn, n_launch, reps, flush):
+    """Device time per launch of a CUDA graph of fn() (n_launch GEMMs), L2 flushed (256 MB write) before
+    every replay, CUDA events on the launching stream around the replay only; median over reps."""
+    fn()
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=stream):
+        fn()
+    gr.replay()
+    ts = []
+    for r in range(reps):
+        flush.fill_(r & 255)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        gr.replay()
+        b.record(stream)
+        ts.append((a, b))
+    torch.cuda.synchronize()
+    return statistics.median(x.elapsed_time(y) for x, y in ts) * 1e3 / n_launch
+
+
+def _int8_peak(torch, dev):
+    """Measured dense int8 tensor peak: cuBLAS INT8 (torch._int_mm) 8192^3, best of 10 (burst)."""
+    a = torch.randint(-8, 8, (8192, 8192), device=dev, dtype=torch.int8)
+    b = torch.randint(-8, 8, (8192, 8192), device=dev, dtype=torch.int8).t()
+    for _ in range(3):
+        torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+def run_legs(args, torch, P, dev, stream, world, rank, barrier, legs):
+    """configs[2] (Llama-2-7B prefill, M = 2048, W2A8 / W4A4, next to cuBLAS INT8 / FP16), configs[3]
+    (Llama-3-70B linears, M = 4096, W2A4, N-split over the ranks: GEMM only and GEMM + all-gather, with the
+    NVLink ingress bound) and configs[4] (4096^3 for all 64 (p_w, p_a)), every GEMM in the selector's
+    config (autotuned table), fp16 epilogue with per-channel and per-token scales.  Tensor-bound: roofline =
+    achieved TOPS / the measured int8 peak (cuBLAS _int_mm 8192^3, this run; x2 nominal for kind::mxf4)."""
+    out = {}
+    g = torch.Generator(device=dev)
+    g.manual_seed(424242 + rank)
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    peak = _int8_peak(torch, dev)
+    out["int8_peak"] = {"TOPS": round(peak, 1), "how": "cuBLAS INT8 torch._int_mm 8192^3, best of 10 (burst), this run"}
+
+    def codes(rows, k, bits):
+        return torch.randint(-(1 << (bits - 1)), 1 << (bits - 1), (rows, k), generator=g, device=dev, dtype=torch.int8)
+
+    def scales(n, lo, hi):
+        return torch.exp2(torch.empty(n, device=dev).uniform_(lo, hi, generator=g)).float()
+
+    def ours(m, n, k, wb, ab, copies=2):
+        Ws = [P.pack(codes(n, k, wb), wb, tiled=True) for _ in range(copies)]
+        a_codes = codes(m, k, ab)
+        A = P.pack(a_codes, ab, digits=True)
+        wsc, asc = scales(n, -10, -6), scales(m, -6, -2)
+        o = torch.empty((m, n), dtype=torch.float16, device=dev)
+        cfg = P.select_config(m, n, k, wb, ab)
+
+        def fn():
+            for W in Ws:
+                P.gemm(W, A, out_kind="f16", w_scale=wsc, a_scale=asc, out=o, config=cfg)
+        us = _chain_us(torch, stream, fn, len(Ws), 5, flush)
+        pack_us = _chain_us(torch, stream, lambda: P.pack(a_codes, ab, out=A), 1, 5, flush)
+        del Ws
+        return us, pack_us, cfg
+
+    if "prefill" in legs and world == 1:
+        rows = []
+        for (wb, ab) in ((2, 8), (4, 4)):
+            for (n, k) in SHAPES:
+                m = 2048
+                us, pack_us, cfg = ours(m, n, k, wb, ab)
+                ops = 2 * m * n * k
+                a8 = torch.randint(-8, 8, (m, k), device=dev, dtype=torch.int8)
+                w8 = torch.randint(-8, 8, (n, k), device=dev, dtype=torch.int8)
+                int8_us = _chain_us(torch, stream, lambda: torch._int_mm(a8, w8.t()), 1, 5, flush)
+                a16 = torch.randn((m, k), device=dev, dtype=torch.float16)
+                w16 = torch.randn((n, k), device=dev, dtype=torch.float16)
+                fp16_us = _chain_us(torch, stream, lambda: torch.matmul(a16, w16.t()), 1, 5, flush)
+                del a8, w8, a16, w16
+                tops = ops / us / 1e6
+                mx = cfg["mma_kind"] == 1
+                rows.append({"case": f"M{m} N{n} K{k} W{wb}A{ab}", "us": round(us, 2), "eff_tops": round(tops, 1),
+                             "act_pack_us": round(pack_us, 2), "tops_incl_pack": round(ops / (us + pack_us) / 1e6, 1),
+                             "cublas_int8_us": round(int8_us, 2), "cublas_fp16_us": round(fp16_us, 2),
+                             "speedup_vs_int8": round(int8_us / us, 3), "speedup_vs_fp16": round(fp16_us / us, 3),
+                             "tensor_frac": round(tops / (peak * (2 if mx else 1)), 4),
+                             "kernel": "tcgen05 kind::mxf4" if mx else "tcgen05 kind::i8", "bn": cfg["bn"]})
+        tot_ops = sum(2 * 2048 * n * k for _ in range(2) for (n, k) in SHAPES)
+        tot_us = sum(r["us"] for r in rows)
+        out["prefill"] = {"workload": "BASELINE configs[2]: Llama-2-7B prefill M=2048, W2A8 and W4A4",
+                          "eff_tops": round(tot_ops / tot_us / 1e6, 1),
+                          "speedup_vs_int8": round(sum(r["cublas_int8_us"] for r in rows) / tot_us, 3),
+                          "speedup_vs_fp16": round(sum(r["cublas_fp16_us"] for r in rows) / tot_us, 3),
+                          "timing": "2 packed-weight copies chained per CUDA graph, 256 MB L2 flush before each replay",
+                          "cases": rows}
+
+    if "llama70b" in legs:
+        rows = []
+        m, k, wb, ab = 4096, 8192, 2, 4
+        for n_total in (8192, 28672):
+            n = n_total // world
+            us, pack_us, cfg = ours(m, n, k, wb, ab, copies=2)
+            gather_us = None
+            if world > 1:
+                import torch.distributed as dist
+                from paper_2508_19087_b200 import tp
+                chunks = 4
+                W = P.pack(codes(n, k, wb), wb, tiled=True)
+                A = [P.pack(codes(m // chunks, k, ab), ab, digits=True) for _ in range(chunks)]
+                wsc, asc = scales(n, -10, -6), scales(m, -6, -2)
+                yt = torch.empty((chunks, n_total, m // chunks), dtype=torch.float16, device=dev)
+                for _ in range(2):
+                    tp.tp_gemm(W, A, n_total, out_kind="f16", w_scale_local=wsc, a_scale=asc, m_chunks=chunks, out=yt)
+                barrier()
+                ts = []
+                for r in range(5):
+                    flush.fill_(r & 255)
+                    barrier()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    tp.tp_gemm(W, A, n_total, out_kind="f16", w_scale_local=wsc, a_scale=asc, m_chunks=chunks, out=yt)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1) * 1e3)
+                t = torch.tensor([statistics.median(ts), us], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                gather_us, us = float(t[0]), float(t[1])
+                del W, A, yt
+            ops = 2 * m * n_total * k
+            ingress_us = (world - 1) / world * 2 * m * n_total / 770e9 * 1e6 if world > 1 else None
+            rows.append({"case": f"M{m} N{n_total} K{k} W{wb}A{ab}", "n_per_rank": n,
+                         "gemm_us": round(us, 2), "gemm_eff_tops": round(ops / us / 1e6, 1),
+                         "gemm_tensor_frac_per_gpu": round(ops / world / us / 1e6 / peak, 4),
+                         "gemm_gather_us": round(gather_us, 2) if gather_us else None,
+                         "gemm_gather_eff_tops": round(ops / gather_us / 1e6, 1) if gather_us else None,
+                         "ingress_bound_us": round(ingress_us, 1) if ingress_us else None,
+                         "kernel": "tcgen05 kind::mxf4" if cfg["mma_kind"] == 1 else "tcgen05 kind::i8"})
+        out["llama70b_tp"] = {"workload": f"BASELINE configs[3]: Llama-3-70B linears M=4096 W2A4, N-split over {world} "
+                                          "GPU(s), column-layout slices, NCCL all-gather of 4 M-chunks overlapped "
+                                          "with the next chunk's GEMM (N>1)",
+                              "ingress": "(P-1)/P x 2 M N bytes at the measured 770 GB/s per direction (B200_PROFILING)",
+                              "timing": "device time, max over ranks", "cases": rows}
+
+    if "sweep" in legs and world == 1:
+        n = m = k = 4096
+        Ws = {wb: [P.pack(codes(n, k, wb), wb, tiled=True) for _ in range(2)] for wb in range(1, 9)}
+        As = {ab: P.pack(codes(m, k, ab), ab, digits=True) for ab in range(1, 9)}
+        wsc, asc = scales(n, -10, -6), scales(m, -6, -2)
+        o = torch.empty((m, n), dtype=torch.float16, device=dev)
+        res, kinds = {}, {}
+        for wb in range(1, 9):
+            for ab in range(1, 9):
+                cfg = P.select_config(m, n, k, wb, ab)
+
+                def fn(wb=wb, ab=ab, cfg=cfg):
+                    for W in Ws[wb]:
+                        P.gemm(W, As[ab], out_kind="f16", w_scale=wsc, a_scale=asc, out=o, config=cfg)
+                us = _chain_us(torch, stream, fn, 2, 3, flush)
+                res[f"W{wb}A{ab}"] = round(2 * m * n * k / us / 1e6, 1)
+                kinds[f"W{wb}A{ab}"] = ("mxf4" if cfg["mma_kind"] == 1 else "i8") + f"/bn{cfg['bn']}"
+        vals = list(res.values())
+        out["sweep"] = {"workload": "BASELINE configs[4]: 4096^3, W1-W8 x A1-A8, selector (autotuned table) config",
+                        "eff_tops": res, "config": kinds, "min_tops": min(vals), "max_tops": max(vals),
+                        "tensor_frac_max": round(max(vals) / peak, 4),
+                        "timing": "2 packed-weight copies chained per CUDA graph, L2 flushed before each replay"}
+        del Ws, As
+    del flush
+    return out
 
 
 def breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, shard, layout, use_graphs, hbm_peak):

@@ -35,54 +35,70 @@ def _all_gather_rows(out_full: torch.Tensor, local: torch.Tensor, group=None):
         dist.all_gather(parts, local, group=group)
 
 
-def tp_gemm(W_local: api.Packed, A: api.Packed, n_total: int, out_kind: str = "i32",
+def tp_gemm(W_local: api.Packed, A, n_total: int, out_kind: str = "i32",
             w_scale_local: torch.Tensor | None = None, a_scale: torch.Tensor | None = None,
-            group=None, m_chunks: int = 1, local_gemm=None) -> torch.Tensor:
-    """Y^T [n_total, M] = gather over ranks of (A . W_r^T)^T.
+            group=None, m_chunks: int = 1, local_gemm=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Gathered Y^T over the ranks' weight-row slices: (A . W_r^T)^T stacked in rank order.
 
-    ``local_gemm(W_local, A_chunk_rows, out_kind, w_scale_local, a_scale_chunk) -> [N/P, m]`` is the
-    per-rank compute; it defaults to the CUDA kernel (api.gemm, column layout).  Tests on CPU
-    inject the oracle here to exercise the sharding and collective logic with gloo.
+    ``A`` is one Packed activation [M, K] or a list of ``m_chunks`` Packed row chunks of equal size (pack
+    the chunks directly to avoid the plane copies ``Packed.narrow_rows`` makes).  Returns Y^T [n_total, M]
+    for one chunk, else the chunk-major [m_chunks, n_total, M / m_chunks]: chunk c's gather lands in its own
+    contiguous block, so there is no permute or copy pass, and the gather of chunk c runs on a
+    side stream while the GEMM of chunk c + 1 computes.
+
+    ``local_gemm(W_local, A_chunk, out_kind, w_scale_local, a_scale_chunk) -> [N/P, m]`` is the per-rank
+    compute; it defaults to the CUDA kernel (api.gemm, column layout).  Tests on CPU inject the oracle here
+    to exercise the sharding and collective logic with gloo.
     """
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     n_local = W_local.rows
     if n_local * world != n_total:
         raise ValueError("W_local rows x world size != n_total")
-    M = A.rows
+    chunks = list(A) if isinstance(A, (list, tuple)) else None
+    if chunks is not None:
+        m_chunks = len(chunks)
+    M = sum(c.rows for c in chunks) if chunks is not None else A.rows
+    m_chunks = max(1, m_chunks)
+    if M % m_chunks != 0:
+        raise ValueError(f"M={M} is not divisible into {m_chunks} equal chunks")
+    mc = M // m_chunks
+    if chunks is None:
+        chunks = [A] if m_chunks == 1 else [A.narrow_rows(c * mc, mc) for c in range(m_chunks)]
+    if any(c.rows != mc for c in chunks):
+        raise ValueError("activation chunks must have equal row counts")
     dtype = torch.float16 if out_kind == "f16" else torch.int32
     device = W_local.planes.device
-    yt = torch.empty((n_total, M), dtype=dtype, device=device)
+    direct = local_gemm is None  # the CUDA kernel can write a single rank's blocks in place
     if local_gemm is None:
         def local_gemm(Wl, Ac, kind, ws, as_):
             return api.gemm(Wl, Ac, out_kind=kind, layout="col", w_scale=ws, a_scale=as_)
-    if m_chunks <= 1 or world == 1:
-        y_local = local_gemm(W_local, A, out_kind, w_scale_local, a_scale)
+    shape = (n_total, M) if m_chunks == 1 else (m_chunks, n_total, mc)
+    if out is None:
+        out = torch.empty(shape, dtype=dtype, device=device)
+    elif tuple(out.shape) != shape or out.dtype != dtype or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous {dtype} tensor of shape {shape}")
+    blocks = [out] if m_chunks == 1 else [out[c] for c in range(m_chunks)]
+    comm = torch.cuda.Stream(device=device) if (device.type == "cuda" and world > 1 and m_chunks > 1) else None
+    for c, A_c in enumerate(chunks):
+        as_c = a_scale[c * mc:(c + 1) * mc] if a_scale is not None else None
         if world == 1:
-            return y_local
-        _all_gather_rows(yt, y_local.contiguous(), group)
-        return yt
-    # chunk M: gather chunk c on a side stream while chunk c+1 computes
-    bounds = [(M * c) // m_chunks for c in range(m_chunks + 1)]
-    comm = torch.cuda.Stream(device=device) if device.type == "cuda" else None
-    pending = []
-    for c in range(m_chunks):
-        m0, m1 = bounds[c], bounds[c + 1]
-        if m1 <= m0:
+            # single rank: the local GEMM writes the block directly
+            if direct:
+                api.gemm(W_local, A_c, out_kind=out_kind, layout="col", w_scale=w_scale_local, a_scale=as_c,
+                         out=blocks[c])
+            else:
+                blocks[c].copy_(local_gemm(W_local, A_c, out_kind, w_scale_local, as_c))
             continue
-        A_c = A.narrow_rows(m0, m1 - m0)
-        y_c = local_gemm(W_local, A_c, out_kind, w_scale_local, a_scale[m0:m1] if a_scale is not None else None)
-        buf = torch.empty((n_total, m1 - m0), dtype=dtype, device=device)
+        y_c = local_gemm(W_local, A_c, out_kind, w_scale_local, as_c)
         if comm is not None:
             ev = torch.cuda.Event()
             ev.record()
             with torch.cuda.stream(comm):
                 comm.wait_event(ev)
-                _all_gather_rows(buf, y_c.contiguous(), group)
+                _all_gather_rows(blocks[c], y_c.contiguous(), group)
+                y_c.record_stream(comm)
         else:
-            _all_gather_rows(buf, y_c.contiguous(), group)
-        pending.append((m0, m1, buf, y_c))
+            _all_gather_rows(blocks[c], y_c.contiguous(), group)
     if comm is not None:
         torch.cuda.current_stream(device).wait_stream(comm)
-    for m0, m1, buf, _ in pending:
-        yt[:, m0:m1].copy_(buf)
-    return yt
+    return out

@@ -47,7 +47,11 @@ def _worker(rank, world, port, m, n, k, wbits, abits, chunks, q):
             return torch.from_numpy(O.gemm_signed(codes_a, codes_w).T.astype(np.int32).copy())
 
         yt = tp.tp_gemm(W_local, A, n, out_kind="i32", m_chunks=chunks, local_gemm=oracle_local)
-        ok = np.array_equal(yt.numpy().astype(np.int64), O.gemm_signed(a, w).T)
+        ref = O.gemm_signed(a, w).T  # [n, m]
+        if chunks > 1:  # chunk-major [chunks, n, m / chunks]: chunk c = columns c*mc .. of Y^T
+            mc = m // chunks
+            ref = np.stack([ref[:, c * mc:(c + 1) * mc] for c in range(chunks)])
+        ok = np.array_equal(yt.numpy().astype(np.int64), ref)
         q.put((rank, bool(ok), tuple(yt.shape)))
     finally:
         dist.destroy_process_group()
@@ -55,7 +59,7 @@ def _worker(rank, world, port, m, n, k, wbits, abits, chunks, q):
 
 @pytest.mark.parametrize("chunks", [1, 3])
 def test_tp_gather_matches_single_device(chunks):
-    world, m, n, k = 2, 7, 64, 300
+    world, m, n, k = 2, 9, 64, 300
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -66,7 +70,7 @@ def test_tp_gather_matches_single_device(chunks):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
-    assert all(shape == (n, m) for _, _, shape in res)
+    assert all(shape == ((n, m) if chunks == 1 else (chunks, n, m // chunks)) for _, _, shape in res)
 
 
 def test_shard_rows():
