@@ -301,6 +301,17 @@ APT_API apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int3
                     void* out, int64_t ldo, const apt_config* cfg, void* workspace, size_t ws_bytes,
                     void* stream);
 
+/* Ablation only (the paper's "Basic" design, §6.5): recovery in global
+ * memory.  parts: int32 [abits * wbits][part_stride], part (i, j) at offset (i * wbits + j) * part_stride
+ * holds the plane-pair product Y^(i,j) = sum_k (2 a_i - 1)(2 w_j - 1) of activation plane i and weight
+ * plane j (e.g. apt_gemm of the 1-bit planes with APT_OUT_I32_BIPOLAR); writes
+ *   out[e] = sum_{i, j} 2^(i + j) parts[(i * wbits + j) * part_stride + e]   (mod 2^32)
+ * for e < count, i.e. the bipolar product Y' of the full codes.  The product path never uses this (its
+ * shift-add is folded into the operand rebuild); it exists to measure what the folding saves.
+ * Errors: APT_ERR_INVALID_ARGUMENT, APT_ERR_CUDA. */
+APT_API apt_status apt_recombine_plane_products(const int32_t* parts, int32_t abits, int32_t wbits, int64_t part_stride,
+                                                int64_t count, int32_t* out, void* stream);
+
 /* Host.  Human-readable name of a status code (static storage). */
 APT_API const char* apt_status_string(apt_status s);
 

@@ -14,8 +14,3 @@ from . import _lib  # noqa: F401
 
 __all__ = ["Packed", "alloc_packed", "gemm", "kpad", "pack", "quantize_pack", "select_config", "workspace_bytes", "default_workspace",
            "load_table", "clear_table", "table_size", "table_lookup", "enumerate_configs", "load_default_table"]
-
-try:  # the shipped autotuned table (NEXT-3); the library itself stays importable without a build
-    load_default_table()
-except ImportError:
-    pass

@@ -21,7 +21,7 @@ APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes", "apt_gemm_zp_workspace_bytes",
             "apt_gemm", "apt_status_string", "apt_abi_version", "apt_table_load", "apt_table_clear", "apt_table_size",
-            "apt_table_lookup", "apt_enumerate_configs"]
+            "apt_table_lookup", "apt_enumerate_configs", "apt_recombine_plane_products"]
 
 
 class AptPacked(ctypes.Structure):
@@ -93,12 +93,20 @@ def lib():
         L.apt_table_size.argtypes = []
         L.apt_table_lookup.restype = ctypes.c_int
         L.apt_table_lookup.argtypes = [ctypes.c_int32] * 5 + [ctypes.POINTER(AptConfig), ctypes.POINTER(ctypes.c_double)]
+        L.apt_recombine_plane_products.restype = ctypes.c_int
+        L.apt_recombine_plane_products.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                                   ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
         L.apt_enumerate_configs.restype = ctypes.c_int32
         L.apt_enumerate_configs.argtypes = [ctypes.c_int32] * 5 + [ctypes.POINTER(AptConfig), ctypes.c_int32]
         v = int(L.apt_abi_version())
         if v != ABI_VERSION:
             raise ImportError(f"{LIB_PATH} has ABI version {v}, this binding needs {ABI_VERSION}: rebuild it")
         _lib = L
+        # the shipped autotuned configuration table (NEXT-3), loaded with the library: APT_TABLE = a path
+        # or "none"; default tables/b200.apt next to this file
+        path = os.environ.get("APT_TABLE", os.path.join(_HERE, "tables", "b200.apt"))
+        if path.lower() != "none" and os.path.exists(path):
+            check("apt_table_load", L.apt_table_load(path.encode()))
     return _lib
 
 

@@ -541,6 +541,16 @@ int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, in
   for (int i = 0; i < n && i < cap && out; ++i) out[i] = v[i];
   return n;
 }
+
+apt_status apt_recombine_plane_products(const int32_t* parts, int32_t abits, int32_t wbits, int64_t part_stride,
+                                        int64_t count, int32_t* out, void* stream) {
+  if (!parts || !out || abits < 1 || abits > 8 || wbits < 1 || wbits > 8 || count <= 0 || part_stride < count)
+    return APT_ERR_INVALID_ARGUMENT;
+  return apt::launch_recombine_planes(parts, abits, wbits, part_stride, count, out,
+                                      reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? APT_OK
+             : APT_ERR_CUDA;
+}
 }  // extern "C"
 
 namespace {

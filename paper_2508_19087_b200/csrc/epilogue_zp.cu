@@ -45,3 +45,34 @@ cudaError_t launch_zp_epilogue(const ZpArgs& p, cudaStream_t stream) {
 }
 
 }  // namespace apt
+
+// ---------------------------------------------------------------------------------------------
+// Recovery in global memory (the paper's "Basic" design, ablation §6.5):
+// the p_a x p_w plane-pair products Y^(i,j) (int32, each from a 1-bit x 1-bit GEMM) are
+// recombined in HBM by the shift-add of P:228,  out = sum_{i<p_a, j<p_w} 2^(i+j) Y^(i,j)  (mod 2^32).
+// The product path never takes this route (its shift-add is folded into the operand rebuild); this
+// kernel exists to measure what that folding saves.
+namespace apt {
+__global__ void __launch_bounds__(256) recombine_planes_kernel(const int32_t* __restrict__ parts, int32_t abits,
+                                                               int32_t wbits, int64_t part_stride, int64_t count,
+                                                               int32_t* __restrict__ out) {
+  pdl_launch_dependents();
+  pdl_wait();  // the plane products come from the GEMMs just before
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+    for (int i = 0; i < abits; ++i)
+      for (int j = 0; j < wbits; ++j)
+        acc += (uint32_t)__ldg(parts + (int64_t)(i * wbits + j) * part_stride + e) << (i + j);
+    out[e] = (int32_t)acc;
+  }
+}
+
+cudaError_t launch_recombine_planes(const int32_t* parts, int abits, int wbits, int64_t part_stride, int64_t count,
+                                    int32_t* out, cudaStream_t stream) {
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  return launch_pdl(recombine_planes_kernel, dim3((unsigned)blocks), dim3(256), 0, stream, dim3(1, 1, 1), parts,
+                    abits, wbits, part_stride, count, out);
+}
+}  // namespace apt

@@ -90,4 +90,7 @@ struct ZpArgs {
   int32_t layout, M, N, K;
 };
 cudaError_t launch_zp_epilogue(const ZpArgs& p, cudaStream_t stream);
+// ablation (the paper's "Basic" recovery in global memory): out = sum_{i,j} 2^(i+j) parts[i * wbits + j]
+cudaError_t launch_recombine_planes(const int32_t* parts, int abits, int wbits, int64_t part_stride, int64_t count,
+                                    int32_t* out, cudaStream_t stream);
 }  // namespace apt

@@ -27,6 +27,9 @@ namespace apt {
 
 constexpr int kPackThreads = 256;
 constexpr int kPackMaxRows = 256;  // rows per CTA (shared row-sum / row-max slots)
+#ifndef APT_PACK_WORD_ROWS
+#define APT_PACK_WORD_ROWS 64  // activation packs up to this many rows take one word per thread
+#endif
 
 // bytewise: signed codes (4 per word) -> offset digits u (4 per word), modulo 2^BITS
 template <int BITS>
@@ -296,7 +299,7 @@ static cudaError_t launch_pack_w(const PackArgs& p, const void* x, float* scale,
 // activation packs (a digit view, few rows) take one word per thread; everything else quads
 template <bool QUANT>
 static cudaError_t launch_pack_t(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {
-  if (p.digits && p.rows <= 64) return launch_pack_w<QUANT, 1>(p, x, scale, bits, stream);
+  if (p.digits && p.rows <= APT_PACK_WORD_ROWS) return launch_pack_w<QUANT, 1>(p, x, scale, bits, stream);
   return launch_pack_w<QUANT, 4>(p, x, scale, bits, stream);
 }
 

@@ -716,3 +716,23 @@ def test_tp_gemm_single_rank_chunked(chunks):
         ref = np.stack([ref[:, c * mc:(c + 1) * mc] for c in range(chunks)])
     assert yt.shape == ref.shape
     assert (np.abs(yt - ref) <= 1e-3 * np.abs(ref) + 2.0 ** -24).all()
+
+
+# ----------------------------------------------------------------------------- ablation: the paper's Basic design (NEXT-4)
+
+@pytest.mark.parametrize("m,n,k,pw,pa", [(16, 256, 700, 2, 2), (5, 130, 300, 3, 4), (300, 200, 1000, 4, 4),
+                                         (16, 64, 256, 8, 8)])
+def test_ablation_basic_plane_pairs(m, n, k, pw, pa):
+    """The Basic design (one 1-bit x 1-bit GEMM per plane pair, recovered in global memory by
+    apt_recombine_plane_products) gives the bipolar product bit for bit — the same result as the
+    fused product path and the oracle's recombination (I1)."""
+    from paper_2508_19087_b200 import ablation
+    a = signed_codes(m, k, pa, seed=401 + m)
+    w = signed_codes(n, k, pw, seed=402 + n)
+    pp = ablation.PlanePairs(_dev(a), pa, _dev(w), pw)
+    got = pp.basic().cpu().numpy().astype(np.int64)
+    ref = O.recombine(O.plane_products(a, pa, w, pw))
+    assert np.array_equal(got, O.gemm_bipolar(a, pa, w, pw))
+    assert np.array_equal(got, ref)
+    A, W = _pack_both(a, pa, w, pw)
+    assert np.array_equal(P.gemm(W, A, out_kind="bipolar").cpu().numpy().astype(np.int64), got)

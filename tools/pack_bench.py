@@ -67,6 +67,15 @@ for key, c in acts.items():
     us = time_graph(one) / 20
     print(json.dumps({"what": "act_pack_b2b", "M": key[0], "abits": key[1], "K": key[2], "us": round(us, 3)}), flush=True)
 
+for (m, k, ab) in [(2048, 4096, 8), (2048, 4096, 4), (2048, 11008, 4), (4096, 8192, 4)]:
+    c = codes(m, k, ab)
+    out = P.alloc_packed(m, k, ab, dev, digits=True)
+    us = time_graph(lambda: P.pack(c, ab, out=out), cold=True)
+    byt = m * k + ab * m * P.kpad(k) // 8 + m * P.kpad(k) + 4 * m
+    print(json.dumps({"what": "act_pack_prefill", "M": m, "K": k, "abits": ab, "us": round(us, 2),
+                      "GB/s": round(byt / us / 1e3, 1)}), flush=True)
+    del c, out
+
 for (n, k) in [(4096, 4096), (11008, 4096), (4096, 11008), (8192, 8192), (28672, 8192)]:
     for wb in [1, 2, 4, 8]:
         c = codes(n, k, wb)
