@@ -282,6 +282,13 @@ __device__ __forceinline__ void epilogue_store_v(const EpilogueArgs& e, int m, i
   }
 }
 
+// two fp32 -> two fp16 (round to nearest even each, IEEE overflow to inf), low half = a
+__device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+
 __device__ __forceinline__ void epilogue_store(const EpilogueArgs& e, int m, int n, uint32_t U) {
   epilogue_store_v(e, m, n, U, __ldg(e.a_rowsum + m), __ldg(e.w_rowsum + n),
                    e.kind == 2 ? __ldg(e.w_scale + n) : 0.f, (e.kind == 2 && e.a_scale) ? __ldg(e.a_scale + m) : 1.f);

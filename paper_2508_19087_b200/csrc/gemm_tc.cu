@@ -670,10 +670,47 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
           for (int jj = 0; jj < kChunk; ++jj) acc[jj] = (uint32_t)__float2int_rn(__uint_as_float(acc[jj]));
         }
         if (n < p.e.N) {
+          if (p.e.kind == 2) {
+            // fp16 (the common case): the rank-1 terms of the row hoisted, one fp32 expression per
+            // element, then either 2-byte stores (row layout: the warp's lanes are consecutive n, so
+            // each store instruction is coalesced) or 16-byte stores of 8 tokens (column layout)
+            const uint32_t cn = (uint32_t)p.e.h_a * (uint32_t)rw + (uint32_t)p.e.kpad * (uint32_t)p.e.h_a * (uint32_t)p.e.h_w;
+            const int mb = m0 + c0;
+            uint32_t hv[kChunk / 2];
 #pragma unroll
-          for (int jj = 0; jj < kChunk; ++jj) {
-            const int m = m0 + c0 + jj;
-            if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[jj], ep_ra[c0 + jj], rw, wsc, ep_as[c0 + jj]);
+            for (int jj = 0; jj < kChunk; jj += 2) {
+              float v2[2];
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2) {
+                const uint32_t y = acc[jj + e2] - (uint32_t)p.e.h_w * (uint32_t)ep_ra[c0 + jj + e2] - cn;
+                v2[e2] = ((float)(int32_t)y * wsc) * ep_as[c0 + jj + e2];
+              }
+              hv[jj / 2] = pack_f16x2(v2[0], v2[1]);
+            }
+            unsigned short* outh = reinterpret_cast<unsigned short*>(p.e.out);
+            if (p.e.layout == 0) {
+              unsigned short* q = outh + (int64_t)mb * p.e.ldo + n;
+#pragma unroll
+              for (int jj = 0; jj < kChunk; ++jj)
+                if (mb + jj < p.e.M) q[(int64_t)jj * p.e.ldo] = (unsigned short)(hv[jj / 2] >> (16 * (jj & 1)));
+            } else {
+              unsigned short* q = outh + (int64_t)n * p.e.ldo + mb;
+              if (mb + kChunk <= p.e.M && ((reinterpret_cast<uintptr_t>(q) & 15u) == 0)) {
+#pragma unroll
+                for (int jj = 0; jj < kChunk; jj += 8)
+                  *reinterpret_cast<uint4*>(q + jj) = make_uint4(hv[jj / 2], hv[jj / 2 + 1], hv[jj / 2 + 2], hv[jj / 2 + 3]);
+              } else {
+#pragma unroll
+                for (int jj = 0; jj < kChunk; ++jj)
+                  if (mb + jj < p.e.M) q[jj] = (unsigned short)(hv[jj / 2] >> (16 * (jj & 1)));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < kChunk; ++jj) {
+              const int m = m0 + c0 + jj;
+              if (m < p.e.M) epilogue_store_v(p.e, m, n, acc[jj], ep_ra[c0 + jj], rw, wsc, ep_as[c0 + jj]);
+            }
           }
         }
       }

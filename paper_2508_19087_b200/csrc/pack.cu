@@ -27,6 +27,9 @@ namespace apt {
 
 constexpr int kPackThreads = 256;
 constexpr int kPackMaxRows = 256;  // rows per CTA (shared row-sum / row-max slots)
+#ifndef APT_PACK_TILED_ROWS
+#define APT_PACK_TILED_ROWS 16  // rows per CTA of a tile-major (weight) pack: one or a few quads per thread
+#endif
 #ifndef APT_PACK_WORD_ROWS
 #define APT_PACK_WORD_ROWS 64  // activation packs up to this many rows take one word per thread
 #endif
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
 // store is 32 consecutive rows of one 16-byte column; otherwise enough rows to give every thread an item
 static int pack_rows_per_cta(const PackArgs& p, int wpi) {
   const int Q = p.k_words / wpi;
-  if (p.tiled && wpi == 4) return 32;
+  if (p.tiled && wpi == 4) return APT_PACK_TILED_ROWS;
   int R = kPackThreads / (Q > 0 ? Q : 1);
   if (R < 1) R = 1;
   if (R > kPackMaxRows) R = kPackMaxRows;

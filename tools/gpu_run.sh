@@ -1,6 +1,6 @@
 # GPU session script (edited per call)
 set -x
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q -k "ablation" 2>&1 | tail -3 > gpurun_out/r2_abl_test.txt
-timeout 600 python tools/ablation.py > gpurun_out/r2_ablation.jsonl 2>&1
-cat gpurun_out/r2_abl_test.txt gpurun_out/r2_ablation.jsonl
+timeout 1500 python tools/tune.py --set prefill,70b,sweep --log gpurun_out/r2_tune_log4.jsonl > gpurun_out/r2_tune4.jsonl 2>&1
+cp paper_2508_19087_b200/tables/b200.apt gpurun_out/b200.apt
+tail -2 gpurun_out/r2_tune4.jsonl

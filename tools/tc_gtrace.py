@@ -25,6 +25,8 @@ if len(sys.argv) > 6:
     cfg["split_k"] = int(sys.argv[6])
 if len(sys.argv) > 7:
     cfg["bn"] = int(sys.argv[7])
+    cfg = [c for c in P.enumerate_configs(m, n, k, wb, ab) if c["kernel"] == 2 and c["bn"] == cfg["bn"]
+           and c["split_k"] == cfg["split_k"] and c["cluster_n"] == 1 and c["mma_kind"] == 0][0]
 out = torch.empty((m, n), dtype=torch.float16, device=dev)
 flush = torch.ones(64 << 20, dtype=torch.int32, device=dev)  # 256 MB, flushed by READING it (clean L2)
 print("cfg", cfg)
@@ -32,6 +34,8 @@ names = ["entry", "prefetch", "w4start", "alloc0", "alloc1", "setup", "firstW", 
 cols = [0, 8, 12, 10, 11, 1, 2, 3, 4, 5, 9, 6]
 for rep in range(4):
     fsum = flush.sum()
+    P._lib.lib().apt_debug_tc_gtrace_reset()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     P.gemm(Ws[rep % 2], A, out_kind="f16", w_scale=ws, out=out, config=cfg)
