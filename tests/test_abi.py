@@ -74,7 +74,8 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab, table_mode):
     assert c.as_dict() == c2.as_dict()
     kw = -(-K // 256) * 8
     assert c.w_digit == wb and c.a_digit == ab
-    assert c.mma_kind == L.APT_MMA_I8
+    assert c.mma_kind == L.APT_MMA_I8 or (c.mma_kind == L.APT_MMA_MXF4 and wb <= 3 and ab <= 3
+                                          and c.kernel == L.APT_KERNEL_TC and table_mode == "table")
     if c.kernel == L.APT_KERNEL_GEMV:
         assert M <= 2 and c.bm == 32 and c.bn == M and c.split_k in (8, 16) and c.stages == 1
         assert c.cluster_n == 1 and c.cta_pair == 0
