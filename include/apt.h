@@ -192,7 +192,7 @@ typedef enum {
                                 rebuilt in registers, tokens from the digit view), 16 weight rows x
                                 bn (8 or 16) tokens x all of K per CTA (bm = 16, bk = 256,
                                 split_k = 4, 8 or 16 warps splitting K, stages = 1)                */
-  APT_KERNEL_DEC = 5         /* M <= 16: mma.sync m16n8k32 u8 with the WEIGHTS as the streamed B operand
+  APT_KERNEL_DEC = 5,        /* M <= 16: mma.sync m16n8k32 u8 with the WEIGHTS as the streamed B operand
                                 (8 rows x 32 K per instruction) and the tokens as the A operand (held in
                                 registers, loaded from a per-CTA shared-memory slab); weights copied into a
                                 per-lane shared-memory ring with cp.async.  bm = 128 weight rows per CTA of
@@ -201,6 +201,10 @@ typedef enum {
                                 16 blocks of 256 K per CTA; > 1 uses the workspace: int32 partials + one
                                 ticket per row tile, see apt_gemm_workspace_bytes).  Needs
                                 Kpad * 255 * 255 < 2^32 (digits are rebuilt as u * 2^s). */
+  APT_KERNEL_PF = 6          /* persistent tcgen05 GEMM for token-rich shapes: one CTA per SM walks the 128 x 128
+                                tiles, every ring continues across tiles, the TMEM accumulator is double-buffered
+                                so dedicated epilogue warps overlap the next tile's MMAs.  bm = bn = 128, bk 128,
+                                stages 6, split_k 1, cluster_n 1; mma_kind i8 or mxf4 (wbits, abits <= 3).    */
 } apt_kernel;
 
 /* Kernel configuration (the B200 analogue of the paper's tunable hyperparameters, §5.1).

@@ -6,7 +6,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libapt.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["apt.cu", "pack.cu", "gemm_tc.cu", "gemv.cu", "gemm_skinny.cu", "gemm_dec.cu", "epilogue_zp.cu"]
+SOURCES = ["apt.cu", "pack.cu", "gemm_tc.cu", "gemv.cu", "gemm_skinny.cu", "gemm_dec.cu", "gemm_pf.cu", "epilogue_zp.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I" + os.path.join(HERE, "..", "include")]

@@ -14,7 +14,7 @@ APT_OK, APT_ERR_INVALID_ARGUMENT, APT_ERR_UNSUPPORTED, APT_ERR_WORKSPACE, APT_ER
 APT_ENC_SIGNED, APT_ENC_BIPOLAR = 0, 1
 APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
 APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
-APT_KERNEL_AUTO, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY, APT_KERNEL_DEC = 0, 2, 3, 4, 5
+APT_KERNEL_AUTO, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY, APT_KERNEL_DEC, APT_KERNEL_PF = 0, 2, 3, 4, 5, 6
 APT_MMA_I8, APT_MMA_MXF4 = 0, 1
 ABI_VERSION = 4  # include/apt.h APT_ABI_VERSION this binding marshals for
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1

@@ -64,6 +64,16 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
   const int kw = (int)(kpad_of(K) / 32);
   if (c->w_digit != wbits || c->a_digit != abits) return APT_ERR_UNSUPPORTED;  // full-width digits only
   if (c->mma_kind != APT_MMA_I8 && c->mma_kind != APT_MMA_MXF4) return APT_ERR_UNSUPPORTED;
+  if (c->kernel == APT_KERNEL_PF) {
+    if (c->bm != 128 || c->bn != 128 || c->bk != 128 || c->stages != 6 || c->split_k != 1 || c->cluster_n != 1 ||
+        c->cta_pair != 0)
+      return APT_ERR_UNSUPPORTED;
+    if (c->mma_kind == APT_MMA_MXF4 && (wbits > 3 || abits > 3 || kpad_of(K) * 16ll >= (1ll << 24)))
+      return APT_ERR_UNSUPPORTED;
+    // i8: weight digits scaled by 2^s (<= 255 each) accumulate in s32: Kpad * 255 * 255 < 2^31
+    if (c->mma_kind == APT_MMA_I8 && kpad_of(K) * 255ll * 255ll >= (1ll << 31)) return APT_ERR_UNSUPPORTED;
+    return APT_OK;
+  }
   if (c->mma_kind == APT_MMA_MXF4) {
     // signed e2m1 digits: codes of at most 3 bits; the tcgen05 prefill tile, one K range, no cluster;
     // f32 accumulation exact while every partial sum is an integer below 2^24 (|x y| <= 16)
@@ -530,6 +540,13 @@ int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, in
   for (int bn : {16, 64, 128, 256})
     for (int cn : {1, 2, 4})
       for (int sp = 1; sp <= 8; ++sp) add(APT_KERNEL_TC, 128, bn, 128, apt::tc_stages(wbits, bn), sp, cn);
+  for (int mk : {APT_MMA_I8, APT_MMA_MXF4}) {  // the persistent tile
+    apt_config c;
+    std::memset(&c, 0, sizeof(c));
+    c.kernel = APT_KERNEL_PF; c.w_digit = wbits; c.a_digit = abits; c.bm = 128; c.bn = 128; c.bk = 128;
+    c.stages = 6; c.split_k = 1; c.cluster_n = 1; c.mma_kind = mk;
+    if (validate_config(&c, M, N, K, wbits, abits) == APT_OK) v.push_back(c);
+  }
   for (int bn : {128, 256}) {  // kind::mxf4 (wbits, abits <= 3)
     apt_config c;
     std::memset(&c, 0, sizeof(c));
@@ -558,6 +575,30 @@ apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_pa
                           int32_t M, int32_t N, int32_t wbits, int32_t abits, void* workspace, cudaStream_t s) {
   // the TC kernel reads the activation operand as kernel-order u8 digits: the packed view, or
   // expanded now into the workspace
+  if (c.kernel == APT_KERNEL_PF) {
+    apt::TcArgs p;
+    p.wp = W->planes;
+    p.w_tiled = W->layout == APT_PACK_TILED ? 1 : 0;
+    p.w_pstride = (int64_t)(p.w_tiled ? (N + 127) / 128 * 128 : N) * W->k_words;
+    p.k_words = W->k_words;
+    p.e = e;
+    const bool mx = c.mma_kind == APT_MMA_MXF4;
+    if (mx || !A->digits) {
+      if (A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
+      uint8_t* xp = reinterpret_cast<uint8_t*>(workspace) + APT_WS_TICKET_BYTES;
+      cudaError_t err = mx ? apt::launch_expand_tokens_mx(A->planes, (int64_t)M * A->k_words, M, A->k_words, abits, xp, s)
+                           : apt::launch_expand_tokens(A->planes, (int64_t)M * A->k_words, M, A->k_words, abits, xp, s);
+      if (err != cudaSuccess) return APT_ERR_CUDA;
+      p.adig = xp;
+    } else {
+      p.adig = A->digits;
+    }
+    if (mx) {
+      p.e.h_w = 0;
+      p.e.h_a = 0;
+    }
+    return apt::launch_gemm_pf(p, wbits, mx ? 1 : 0, s) == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+  }
   if (c.mma_kind == APT_MMA_MXF4) {
     // kind::mxf4: tokens as signed e2m1 nibbles, expanded from the activation planes into the workspace;
     // the f32 accumulator is already the signed product (no offset-digit correction: h_w = h_a = 0)

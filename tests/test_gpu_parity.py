@@ -736,3 +736,47 @@ def test_ablation_basic_plane_pairs(m, n, k, pw, pa):
     assert np.array_equal(got, ref)
     A, W = _pack_both(a, pa, w, pw)
     assert np.array_equal(P.gemm(W, A, out_kind="bipolar").cpu().numpy().astype(np.int64), got)
+
+
+# ----------------------------------------------------------------------------- persistent tcgen05 tile (APT_KERNEL_PF)
+
+def _pf_cfg(m, n, k, wb, ab, mx=0):
+    return dict(P.select_config(m, n, k, wb, ab), kernel=6, bm=128, bn=128, bk=128, stages=6, split_k=1, cta_pair=0,
+                cluster_n=1, mma_kind=mx)
+
+
+@pytest.mark.parametrize("pw,pa,mx", [(1, 1, 0), (2, 8, 0), (4, 4, 0), (5, 3, 0), (8, 8, 0), (3, 3, 1), (1, 2, 1), (2, 3, 1)])
+@pytest.mark.parametrize("tiled", [True, False])
+def test_pf_matches_oracle(pw, pa, mx, tiled):
+    """APT_KERNEL_PF (i8 and mxf4): int32 signed / bipolar bit-exact and fp16 within 1e-3 on ragged shapes
+    (M, N not multiples of 128, K not a multiple of 256, more tiles than SMs and fewer), row and column
+    layouts, tile-major and canonical weights, with and without the activation digit view."""
+    for m, n, k in ((300, 333, 700), (129, 130, 1300), (2048, 1100, 512), (70, 40, 256)):
+        a = signed_codes(m, k, pa, seed=510 + pa + m)
+        w = signed_codes(n, k, pw, seed=520 + pw + n)
+        A = P.pack(_dev(a), pa, digits=(m % 2 == 0))
+        W = P.pack(_dev(w), pw, tiled=tiled)
+        cfg = _pf_cfg(m, n, k, pw, pa, mx)
+        ref = O.gemm_signed(a, w)
+        assert np.array_equal(P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64), ref)
+        got = P.gemm(W, A, out_kind="bipolar", layout="col", config=cfg).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got.T, ref * 4 + 2 * a.astype(np.int64).sum(1)[:, None] + 2 * w.astype(np.int64).sum(1)[None, :] + k)
+        ws = log_uniform_scales(n, -10, -6, seed=35)
+        as_ = log_uniform_scales(m, -6, -2, seed=36)
+        r = O.scale_fp64(ref, ws, as_)
+        for lay in ("row", "col"):
+            got = P.gemm(W, A, out_kind="f16", layout=lay, w_scale=_dev(ws), a_scale=_dev(as_), config=cfg).cpu().numpy()
+            got = (got if lay == "row" else got.T).astype(np.float64)
+            assert (np.abs(got - r) <= 1e-3 * np.abs(r) + 2.0 ** -24).all()
+
+
+@pytest.mark.parametrize("n,k", LLAMA7B)
+@pytest.mark.parametrize("pw,pa", [(2, 8), (4, 4)])
+def test_pf_llama7b_prefill_full(n, k, pw, pa):
+    """BASELINE configs[2] at full size through APT_KERNEL_PF: EVERY output element vs the oracle."""
+    m = 2048
+    a = signed_codes(m, k, pa, seed=config_seed(2, pw, pa, salt=13))
+    w = signed_codes(n, k, pw, seed=config_seed(2, pw, pa, salt=13) + 1)
+    A, W = _pack_both(a, pa, w, pw)
+    got = P.gemm(W, A, config=_pf_cfg(m, n, k, pw, pa)).cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, O.gemm_signed_blas(a, w))

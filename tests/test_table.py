@@ -104,7 +104,7 @@ def test_enumeration_is_the_legal_space(empty_table, m, n, k, wb, ab):
     for c in space[:: max(1, len(space) // 12)]:
         assert c["w_digit"] == wb and c["a_digit"] == ab
         if m <= 16:
-            assert all(x["kernel"] in (2, 3, 4, 5) for x in space)
+            assert all(x["kernel"] in (2, 3, 4, 5, 6) for x in space)
     assert P.enumerate_configs(2, 33025, 33025, 8, 8) == []  # int32 bound (reading Q8)
 
 
