@@ -75,7 +75,7 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab, table_mode):
     kw = -(-K // 256) * 8
     assert c.w_digit == wb and c.a_digit == ab
     assert c.mma_kind == L.APT_MMA_I8 or (c.mma_kind == L.APT_MMA_MXF4 and wb <= 3 and ab <= 3
-                                          and c.kernel == L.APT_KERNEL_TC and table_mode == "table")
+                                          and c.kernel in (L.APT_KERNEL_TC, L.APT_KERNEL_PF) and table_mode == "table")
     if c.kernel == L.APT_KERNEL_GEMV:
         assert M <= 2 and c.bm == 32 and c.bn == M and c.split_k in (8, 16) and c.stages == 1
         assert c.cluster_n == 1 and c.cta_pair == 0
@@ -84,6 +84,8 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab, table_mode):
         assert c.split_k in (4, 8, 16) and c.stages == 1 and c.cluster_n == 1 and c.cta_pair == 0
         if table_mode == "analytic":
             assert 2 < M <= 8 and K <= 4096 and c.bn == 8 and c.split_k in (4, 8)
+    elif c.kernel == L.APT_KERNEL_PF:
+        assert table_mode == "table" and c.bm == 128 and c.bn == 128 and c.split_k == 1 and c.cluster_n == 1
     elif c.kernel == L.APT_KERNEL_DEC:
         assert table_mode == "table" and M <= 16 and c.bm == 32 and c.bn == (8 if M <= 8 else 16) and c.bk == 256
         assert c.stages in (4, 8) and 1 <= c.split_k <= 32 and c.cluster_n == 1 and c.cta_pair == 0
