@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
         for (int c = 0; c < chunks; ++c, ++gc) {
           const int slot = gc % WS;
           mbar_wait(wempty(slot), ((gc / WS) & 1) ^ 1);
+          // the converters' generic-proxy reads of this slot (released through wempty) before the async-proxy
+          // (bulk copy / TMA) overwrite: a proxy fence makes the write-after-read order explicit
+          fence_proxy_async();
           mbar_expect_tx(wfull(slot), (uint32_t)L::kWChunk);
           if (tiled) {
 #pragma unroll

@@ -257,6 +257,9 @@ __global__ void __launch_bounds__(384, (BN <= 128 && WB <= 4) ? 2 : 1) gemm_tc_k
   auto issue_w = [&](int c) {  // weight chunk c (local steps 2c, 2c + 1)
     const int slot = c % L::kWSlots;
     mbar_wait(wempty(slot), ((c / L::kWSlots) & 1) ^ 1);
+    // the converters' generic-proxy reads of this slot (released through wempty) before the async-proxy
+    // (bulk copy / TMA) overwrite: a proxy fence makes the write-after-read order explicit
+    fence_proxy_async();
     if (tiled) {
       const int steps = min(2, nloc - 2 * c);
       mbar_expect_tx(wfull(slot), (uint32_t)(steps * 2048 * WB));
