@@ -17,7 +17,11 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_tensor_cycles_active_realtime", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"]
+        "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "sm__pipe_tensor_cycles_active.avg.pct", "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct",
+        "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct", "sm__pipe_shared_cycles_active.avg.pct",
+        "l1tex__m_xbar2l1tex_read_bytes.sum", "sm__cycles_elapsed.avg.per_second", "smsp__issue_active.avg.pct",
+        "sm__inst_executed_pipe_uniform.avg.pct"]
 for h, u, v in zip(hdr, units, vals):
     if any(h.startswith(w) for w in want):
         print(f"{h:80s} {u:12s} {v}")
