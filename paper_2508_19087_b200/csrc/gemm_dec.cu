@@ -83,7 +83,7 @@ __device__ __forceinline__ unsigned long long dec_gtimer() {
 #endif
 
 template <int WB, int MT, int NW, bool TILED>
-__global__ void __launch_bounds__(32 * NW, NW >= 8 ? 1 : 4) gemm_dec_kernel(DecArgs p) {
+__global__ void __launch_bounds__(32 * NW, NW >= 8 ? 1 : 3) gemm_dec_kernel(DecArgs p) {
   using SH = DecShape<WB, NW>;
   constexpr int D = SH::kD;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -176,8 +176,25 @@ __global__ void __launch_bounds__(32 * NW, NW >= 8 ? 1 : 4) gemm_dec_kernel(DecA
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[q][j] = 0;
-  uint4 tk[MT][4];
-  if (nblk > 0) load_tok(b0, tk);
+  // A fragments of the current block, assembled once per block as aligned quads {a0, a1, a2, a3} =
+  // {row g reg 2s, row g+8 reg 2s, row g reg 2s+1, row g+8 reg 2s+1} of word 2t + c (no register moves
+  // per MMA; rows >= 8 are zero for M <= 8)
+  uint4 af[2][4];
+  auto assemble = [&](const uint4 (&tk)[MT][4]) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const uint32_t* ag = reinterpret_cast<const uint32_t*>(&tk[0][2 * c]);
+      const uint32_t* ah = reinterpret_cast<const uint32_t*>(&tk[MT - 1][2 * c]);
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4)
+        af[c][s4] = make_uint4(ag[2 * s4], MT > 1 ? ah[2 * s4] : 0u, ag[2 * s4 + 1], MT > 1 ? ah[2 * s4 + 1] : 0u);
+    }
+  };
+  if (nblk > 0) {
+    uint4 tk[MT][4];
+    load_tok(b0, tk);
+    assemble(tk);
+  }
 #pragma unroll 1
   for (int bl = 0; bl < nblk; ++bl) {
     uint4 tn[MT][4];
@@ -201,20 +218,12 @@ __global__ void __launch_bounds__(32 * NW, NW >= 8 ? 1 : 4) gemm_dec_kernel(DecA
 #pragma unroll
         for (int i = 0; i < WB; ++i) w[i] = c ? wv[i].y : wv[i].x;
         dec_rebuild<WB>(w, o);
-        const uint32_t* ag = reinterpret_cast<const uint32_t*>(&tk[0][2 * c]);
-        const uint32_t* ah = reinterpret_cast<const uint32_t*>(&tk[MT - 1][2 * c]);
 #pragma unroll
         for (int s4 = 0; s4 < 4; ++s4)
-          mma_u8(acc[q], ag[2 * s4], MT > 1 ? ah[2 * s4] : 0u, ag[2 * s4 + 1], MT > 1 ? ah[2 * s4 + 1] : 0u, o[2 * s4],
-                 o[2 * s4 + 1]);
+          mma_u8(acc[q], af[c][s4].x, af[c][s4].y, af[c][s4].z, af[c][s4].w, o[2 * s4], o[2 * s4 + 1]);
       }
     }
-    if (bl + 1 < nblk) {
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) tk[m][j] = tn[m][j];
-    }
+    if (bl + 1 < nblk) assemble(tn);
   }
   cp_async_wait<0>();
   DTRACE(5);
