@@ -26,6 +26,7 @@
 namespace apt {
 
 constexpr int kPackThreads = 256;
+constexpr int kPackWordThreads = 1024;  // one-word-per-thread activation packs: every item in one round
 constexpr int kPackMaxRows = 256;  // rows per CTA (shared row-sum / row-max slots)
 #ifndef APT_PACK_TILED_ROWS
 #define APT_PACK_TILED_ROWS 16  // rows per CTA of a tile-major (weight) pack: one or a few quads per thread
@@ -139,7 +140,7 @@ __device__ __forceinline__ void load_words(const PackArgs& p, const void* rowp, 
 // WPI = words per work item: 4 (a 128-element quad, one 16-byte store per plane: the weight packs,
 // bandwidth) or 1 (one 32-element word: the activation packs, a short per-thread critical path)
 template <int BITS, bool QUANT, int WPI>
-__global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const __half* __restrict__ x, float* scale,
+__global__ void __launch_bounds__(WPI == 1 ? kPackWordThreads : kPackThreads, WPI == 1 ? 1 : 2) pack_kernel(PackArgs p, const __half* __restrict__ x, float* scale,
                                                              int rows_per_cta) {
   if (p.digits) pdl_launch_dependents();  // activation operand: see pack_release()
   pdl_wait();  // our codes / output buffers may still be in use by the previous kernel
@@ -263,7 +264,19 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
       else
         dst[(int64_t)i * p.plane_stride] = pw[i][0];
     }
-    atomicAdd(&s_sum[rl], sum);
+    if constexpr (WPI == 1) {
+      // one shared atomic per warp when the warp's words share a row (all but row boundaries)
+      const unsigned act = __activemask();
+      const int lead = __ffs(act) - 1;
+      if (__all_sync(act, rl == __shfl_sync(act, rl, lead))) {
+        sum = __reduce_add_sync(act, sum);
+        if ((int)(threadIdx.x & 31) == lead) atomicAdd(&s_sum[rl], sum);
+      } else {
+        atomicAdd(&s_sum[rl], sum);
+      }
+    } else {
+      atomicAdd(&s_sum[rl], sum);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < R; i += blockDim.x)
@@ -276,16 +289,25 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_kernel(PackArgs p, const
 static int pack_rows_per_cta(const PackArgs& p, int wpi) {
   const int Q = p.k_words / wpi;
   if (p.tiled && wpi == 4) return APT_PACK_TILED_ROWS;
+  if (wpi == 1 && Q > kPackThreads) return 1;  // a whole row per CTA, one word per thread (pack_threads)
   int R = kPackThreads / (Q > 0 ? Q : 1);
   if (R < 1) R = 1;
   if (R > kPackMaxRows) R = kPackMaxRows;
   return R;
 }
 
+// threads per CTA: 256, or for a one-word-per-thread pack of a row longer than 256 words, the row's
+// word count (rounded to a warp, at most 1024) so no thread walks two items in series
+static int pack_threads(const PackArgs& p, int wpi) {
+  const int Q = p.k_words / wpi;
+  if (wpi != 1 || Q <= kPackThreads) return kPackThreads;
+  return Q >= kPackWordThreads ? kPackWordThreads : (Q + 31) / 32 * 32;
+}
+
 template <bool QUANT, int WPI>
 static cudaError_t launch_pack_w(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {
   const int R = pack_rows_per_cta(p, WPI);
-  const dim3 grid((p.rows + R - 1) / R), block(kPackThreads);
+  const dim3 grid((p.rows + R - 1) / R), block(pack_threads(p, WPI));
   const __half* xh = reinterpret_cast<const __half*>(x);
   switch (bits) {
     case 1: return launch_pdl(pack_kernel<1, QUANT, WPI>, grid, block, 0, stream, dim3(1, 1, 1), p, xh, scale, R);
