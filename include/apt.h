@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define APT_ABI_VERSION 4
+#define APT_ABI_VERSION 5
 #define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
 
 typedef enum {
@@ -304,6 +304,39 @@ APT_API apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int3
                     const apt_packed* A, const apt_scales* scales, apt_out_kind kind, apt_layout layout,
                     void* out, int64_t ldo, const apt_config* cfg, void* workspace, size_t ws_bytes,
                     void* stream);
+
+/* Grouped decode GEMM: `count` INDEPENDENT W_p x A_q products in one persistent launch (the projections
+ * of a decoder layer that share no data dependency, the experts of a mixture-of-experts layer, a batch of
+ * decode linears).  Each problem's result is bit-identical to apt_gemm on the same arguments (same
+ * digit rebuild, products and epilogue as APT_KERNEL_DEC; P:223-228 for the product, P:201 for the
+ * scales); what differs is the schedule: the warps of one grid split the SUM of all problems' packed
+ * weight blocks (32 rows x 256 K) into equal-cost contiguous ranges (stream-K), so weights stream
+ * through one continuous pipeline with no launch boundary between problems (DESIGN.md §7 "Grouped").
+ * Per problem (apt_gemm_problem, host array):
+ *   M in [1, 16]; W = apt_pack_bipolar output in APT_PACK_TILED layout without a digit view; A = an
+ *   APT_PACK_ROWS activation WITH its digit view; kind / layout / out / ldo / scales as apt_gemm
+ *   (zero points are not supported here: w_zero and a_zero must be NULL); 1 <= wbits, abits <= 8 and
+ *   Kpad * 255 * 255 < 2^32 (the digits are u * 2^s).
+ * The problems must not overlap: no problem's `out` may alias another problem's inputs or output.
+ *   workspace : device, >= apt_gemm_grouped_workspace_bytes(count), 16-byte aligned; its first
+ *               APT_WS_TICKET_BYTES are the same zero-initialised ticket area as apt_gemm's (one
+ *               workspace serves both kinds of call on one stream).
+ * Errors: APT_ERR_INVALID_ARGUMENT (count outside [1, APT_GROUP_MAX], a problem violating the above),
+ *         APT_ERR_UNSUPPORTED (int32 bound), APT_ERR_WORKSPACE, APT_ERR_CUDA. */
+#define APT_GROUP_MAX 64
+typedef struct {
+  int32_t M, N, K, wbits, abits;
+  apt_packed W;
+  apt_packed A;
+  apt_scales scales;
+  int32_t kind;   /* apt_out_kind */
+  int32_t layout; /* apt_layout   */
+  void* out;
+  int64_t ldo;
+} apt_gemm_problem;
+APT_API size_t apt_gemm_grouped_workspace_bytes(int32_t count);
+APT_API apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems /* host */, void* workspace,
+                                    size_t ws_bytes, void* stream);
 
 /* Ablation only (the paper's "Basic" design, §6.5): recovery in global
  * memory.  parts: int32 [abits * wbits][part_stride], part (i, j) at offset (i * wbits + j) * part_stride

@@ -284,3 +284,61 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
                           ctypes.byref(c) if c is not None else None, ws_ptr, ws_len, _stream_handle(stream))
     L.check("apt_gemm", rc)
     return out
+
+
+def grouped_workspace(device) -> torch.Tensor:
+    """A zero-initialised workspace large enough for apt_gemm_grouped (and, since its ticket area is
+    shared, usable by apt_gemm calls on the same stream as well)."""
+    nbytes = int(L.lib().apt_gemm_grouped_workspace_bytes(1))
+    return default_workspace(device, nbytes)
+
+
+def gemm_grouped(problems, workspace: torch.Tensor | None = None, stream=None) -> list:
+    """apt_gemm_grouped: several INDEPENDENT decode GEMMs (M <= 16 each) in one persistent launch.
+
+    ``problems`` is a sequence of dicts with the keys of :func:`gemm`: ``W`` (tile-major Packed),
+    ``A`` (Packed with its digit view), and optionally ``out_kind``, ``layout``, ``w_scale``,
+    ``a_scale``, ``out``.  Returns the list of outputs; each equals ``gemm`` on the same arguments."""
+    problems = list(problems)
+    n = len(problems)
+    if not 1 <= n <= L.APT_GROUP_MAX:
+        raise ValueError(f"apt_gemm_grouped takes 1..{L.APT_GROUP_MAX} problems, got {n}")
+    arr = (L.AptGemmProblem * n)()
+    outs = []
+    dev = None
+    for i, pr in enumerate(problems):
+        W, A = pr["W"], pr["A"]
+        _require_cuda(W.planes, "W.planes")
+        _require_cuda(A.planes, "A.planes")
+        dev = W.planes.device
+        if A.k != W.k:
+            raise ValueError(f"problem {i}: A and W have different K")
+        M, N, K = A.rows, W.rows, W.k
+        kind = _OUT_KINDS[pr.get("out_kind", "i32")]
+        lay = _LAYOUTS[pr.get("layout", "row")]
+        shape = (M, N) if lay == L.APT_LAYOUT_ROW else (N, M)
+        dtype = torch.float16 if kind == L.APT_OUT_F16_SCALED else torch.int32
+        out = pr.get("out")
+        if out is None:
+            out = torch.empty(shape, dtype=dtype, device=dev)
+        if out.dtype != dtype or out.dim() != 2 or out.stride(1) != 1 or tuple(out.shape) != shape:
+            raise ValueError(f"problem {i}: out must be a {dtype} tensor of shape {shape} with unit inner stride")
+        ws_, as_ = pr.get("w_scale"), pr.get("a_scale")
+        for t, nm in ((ws_, "w_scale"), (as_, "a_scale")):
+            if t is not None:
+                _require_cuda(t, nm)
+                if t.dtype != torch.float32 or not t.is_contiguous():
+                    raise ValueError(f"problem {i}: {nm} must be contiguous fp32")
+        p = arr[i]
+        p.M, p.N, p.K, p.wbits, p.abits = M, N, K, W.bits, A.bits
+        p.W, p.A = W.struct(), A.struct()
+        p.scales = L.AptScales(ws_.data_ptr() if ws_ is not None else None, as_.data_ptr() if as_ is not None else None,
+                               None, None)
+        p.kind, p.layout, p.out, p.ldo = kind, lay, out.data_ptr(), out.stride(0)
+        outs.append(out)
+    if workspace is None:
+        workspace = grouped_workspace(dev)
+    rc = L.lib().apt_gemm_grouped(n, arr, workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                  _stream_handle(stream))
+    L.check("apt_gemm_grouped", rc)
+    return outs

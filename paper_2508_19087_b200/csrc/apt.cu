@@ -11,6 +11,7 @@
 
 #include "../../include/apt.h"
 #include "kernels.h"
+#include "sync.cuh"
 
 
 namespace {
@@ -557,6 +558,105 @@ int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, in
   const int n = (int)v.size();
   for (int i = 0; i < n && i < cap && out; ++i) out[i] = v[i];
   return n;
+}
+
+// ---- grouped decode GEMM (include/apt.h apt_gemm_grouped, gemm_grp.cu)
+static int grp_max_workers() { return device_sms() * 3; }  // one worker per CTA, at most 3 CTAs per SM
+
+size_t apt_gemm_grouped_workspace_bytes(int32_t count) {
+  if (count < 1 || count > APT_GROUP_MAX) return 0;
+  // tickets, then int32 partials [worker][2][4 warps][16 x 32]
+  return APT_WS_TICKET_BYTES + (size_t)grp_max_workers() * 2u * 4u * 512u * 4u;
+}
+
+apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems, void* workspace, size_t ws_bytes,
+                            void* stream) {
+  if (count < 1 || count > APT_GROUP_MAX || count > apt::kGrpMax || !problems) return APT_ERR_INVALID_ARGUMENT;
+  static_assert(APT_GROUP_MAX <= apt::kGrpMax, "group size");
+  apt::GrpArgs ga;
+  std::memset(&ga, 0, sizeof(ga));
+  int64_t blocks = 0, cost = 0;
+  int wbmax = 1, cmax = 1;
+  for (int i = 0; i < count; ++i) {
+    const apt_gemm_problem& P = problems[i];
+    const int32_t M = P.M, N = P.N, K = P.K;
+    if (M <= 0 || M > 16 || N <= 0 || K <= 0 || P.wbits < 1 || P.wbits > 8 || P.abits < 1 || P.abits > 8 || !P.out)
+      return APT_ERR_INVALID_ARGUMENT;
+    if (validate_packed(&P.W, N, K, P.wbits) != APT_OK || P.W.layout != APT_PACK_TILED || P.W.digits)
+      return APT_ERR_INVALID_ARGUMENT;
+    if (validate_packed(&P.A, M, K, P.abits) != APT_OK || !P.A.digits || !aligned16(P.A.digits))
+      return APT_ERR_INVALID_ARGUMENT;
+    if (P.kind != APT_OUT_I32_SIGNED && P.kind != APT_OUT_I32_BIPOLAR && P.kind != APT_OUT_F16_SCALED)
+      return APT_ERR_INVALID_ARGUMENT;
+    if (P.layout != APT_LAYOUT_ROW && P.layout != APT_LAYOUT_COL) return APT_ERR_INVALID_ARGUMENT;
+    if (P.layout == APT_LAYOUT_ROW ? P.ldo < N : P.ldo < M) return APT_ERR_INVALID_ARGUMENT;
+    if (P.kind == APT_OUT_F16_SCALED && !P.scales.w_scale) return APT_ERR_INVALID_ARGUMENT;
+    if (P.scales.w_zero || P.scales.a_zero) return APT_ERR_INVALID_ARGUMENT;
+    if (!bound_ok(K, P.wbits, P.abits)) return APT_ERR_UNSUPPORTED;
+    if (kpad_of(K) * 255ll * 255ll >= (1ll << 32)) return APT_ERR_UNSUPPORTED;  // u * 2^s digits (gemm_dec.cu)
+    apt::GrpProblem& q = ga.p[i];
+    {
+      // token digit view [M][Kpad] u8: 128 x M boxes, 128-byte swizzle
+      apt::PFN_encodeTiled_t enc = apt::tensor_map_encoder();
+      if (!enc) return APT_ERR_CUDA;
+      const cuuint64_t kp = (cuuint64_t)P.A.k_words * 32;
+      cuuint64_t dims[2] = {kp, (cuuint64_t)M};
+      cuuint64_t strides[1] = {kp};
+      cuuint32_t box[2] = {128, (cuuint32_t)M};
+      cuuint32_t es[2] = {1, 1};
+      if (enc(&q.tok, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, P.A.digits, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return APT_ERR_INVALID_ARGUMENT;
+    }
+    q.wp = P.W.planes;
+    q.w_pstride = (int64_t)((N + 127) / 128 * 128) * P.W.k_words;
+    q.adig = P.A.digits;
+    apt::EpilogueArgs& e = q.e;
+    e.w_rowsum = P.W.row_sum;
+    e.a_rowsum = P.A.row_sum;
+    e.w_scale = P.scales.w_scale;
+    e.a_scale = P.scales.a_scale;
+    e.out = P.out;
+    e.ldo = P.ldo;
+    e.kind = P.kind;
+    e.layout = P.layout;
+    e.M = M;
+    e.N = N;
+    e.K = K;
+    e.kpad = (int32_t)kpad_of(K);
+    e.h_w = 1 << (P.wbits - 1);
+    e.h_a = 1 << (P.abits - 1);
+    q.k_words = P.W.k_words;
+    q.nb = P.W.k_words / 8;  // units of 128 rows x 256 K per 128-row tile
+    q.tiles = (N + 127) / 128;
+    q.wbits = P.wbits;
+    q.cost = 4 * P.wbits + 2;  // KB of packed weights per unit + a fixed share (tokens, MMAs)
+    q.blk0 = blocks;
+    q.cost0 = cost;
+    blocks += (int64_t)q.tiles * q.nb;
+    cost += (int64_t)q.tiles * q.nb * q.cost;
+    wbmax = std::max(wbmax, P.wbits);
+    cmax = std::max(cmax, q.cost);
+  }
+  // every worker owns at least one block when workers * max cost <= total cost (gemm_grp.cu grp_owner)
+#ifdef APT_GRP_CPS
+  const int cps = APT_GRP_CPS;
+#else
+  const int cps = apt::grp_ctas_per_sm(wbmax);
+#endif
+  int64_t workers = std::min<int64_t>((int64_t)device_sms() * cps, cost / cmax);
+  workers = std::max<int64_t>(workers, 1);
+  if (workers > grp_max_workers() || workers * 4 > APT_WS_TICKETS) return APT_ERR_UNSUPPORTED;  // a ticket per warp slice
+  if (!workspace || ws_bytes < apt_gemm_grouped_workspace_bytes(count) || !aligned16(workspace))
+    return APT_ERR_WORKSPACE;
+  ga.count = count;
+  ga.workers = (int32_t)workers;
+  ga.total_blocks = blocks;
+  ga.total_cost = cost;
+  ga.tickets = reinterpret_cast<uint32_t*>(workspace);
+  ga.partials = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(workspace) + APT_WS_TICKET_BYTES);
+  cudaError_t err = apt::launch_gemm_grp(ga, wbmax, (int)workers, reinterpret_cast<cudaStream_t>(stream));
+  return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
 }
 
 apt_status apt_recombine_plane_products(const int32_t* parts, int32_t abits, int32_t wbits, int64_t part_stride,

@@ -1,0 +1,480 @@
+// gemm_grp.cu — grouped decode GEMM (apt_gemm_grouped): many independent APT W_p x A_q products with
+// M <= 16 tokens each (a decoder layer's projections, the experts of a mixture-of-experts layer, the
+// bench's 36 Llama-2-7B decode linears) in ONE persistent launch.
+//
+// Why: a single decode GEMM streams 2-23 MB of packed weights, i.e. 0.3-3.5 us at HBM speed, while a
+// launch costs ~1 us of prologue and another ~1 us before its first weight bytes arrive
+// (profiles/r2_dec_trace.txt, r2_chain_floor.json); chained, the per-GEMM kernels spend as much time
+// ramping up and draining as streaming.  Here every warp is an independent worker that streams its
+// share of ALL the problems' weights through one continuous shared-memory ring, so HBM never sees a
+// launch boundary inside the group.
+//
+// Work decomposition (stream-K over the group): the unit is a block = 32 weight rows x 256 K elements
+// of one problem (problem-major, then row tile, then K).  Blocks carry a cost (2 p_w + 1: the packed
+// bytes plus a fixed share for the token fragments and MMAs) and every warp takes one contiguous
+// range of equal total cost (midpoint rule, integer arithmetic, so every warp computes every other
+// warp's range without communication).  A warp accumulates consecutive blocks of the same row tile in
+// registers; a tile covered by one warp goes straight to the epilogue, a tile split between warps
+// writes int32 partials ([worker][2][16 x 32]) and the last warp to take the tile's ticket (acq_rel,
+// keyed by the tile's first worker) adds them and runs the epilogue.
+//
+// Per block a lane (g, t) = (lane / 4, lane % 4) computes exactly what gemm_dec.cu computes (same
+// digit rebuild — rebuild_hi / rebuild_x16 / rebuild8, the shift half of the shift-add recovery,
+// P:228 —, the same mma.sync.m16n8k32 u8 fragments with the weights as the B operand and the tokens
+// g, g + 8 of the activation digit view as the A operand, the same rank-1 correction and epilogue);
+// only the weight staging differs: 16-byte cp.async copies of whole 512-byte runs of the tile-major
+// layout, lane = weight row, read back by the MMA lanes after a warp barrier.
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "sync.cuh"
+
+namespace apt {
+
+template <int WBMAX>
+struct GrpShape {
+  // CTA = 4 consumer warps (32 weight rows each) + 1 producer warp; unit = 128 weight rows x 256 K.
+  // Slot = WBMAX weight planes of the unit (4 KB each: the tile-major [half][128 rows][4 words] block,
+  // one contiguous bulk copy per plane) + the unit's token digits (two 2-D TMA boxes of M rows x 128
+  // bytes, 128-byte swizzle: the fragment reads of rows g = 0..7 hit distinct banks).
+  static constexpr int kTok = WBMAX * 4096;
+  static constexpr int kSlot = WBMAX * 4096 + 4096;
+#ifdef APT_GRP_D
+  static constexpr int kD = APT_GRP_D;
+#else
+  static constexpr int kD = WBMAX <= 2 ? 6 : WBMAX <= 4 ? 3 : 3;
+#endif
+  static constexpr int kBarOff = kD * kSlot;
+  static constexpr int kSmem = kBarOff + 2 * kD * 8 + 16;
+};
+
+template <int WB>
+__device__ __forceinline__ void grp_rebuild(const uint32_t* w, uint32_t (&o)[8]) {
+  if constexpr (WB <= 2) rebuild_hi<WB>(w, o);
+  else if constexpr (WB <= 4) rebuild_x16<WB>(w, o);
+  else rebuild8<WB>(w, o);
+}
+// digits are u * 2^shift (gemm_dec.cu DecShape::kShift)
+__device__ __forceinline__ int grp_shift(int wb) { return wb <= 2 ? 8 - wb : wb <= 4 ? 4 : 0; }
+
+__device__ __forceinline__ void grp_mma(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// worker owning block i of problem q (midpoint rule): floor((2 cost0 + (2 i + 1) cost) * W / (2 T))
+__device__ __forceinline__ int grp_owner(const GrpArgs& a, const GrpProblem& q, int64_t i) {
+  return (int)((2 * q.cost0 + (2 * i + 1) * (int64_t)q.cost) * a.workers / (2 * a.total_cost));
+}
+
+// first block (problem p, local index i, global index gi) owned by a worker >= w; p = count if none
+__device__ void grp_find(const GrpArgs& a, int w, int& p_out, int64_t& i_out, int64_t& g_out) {
+  for (int p = 0; p < a.count; ++p) {
+    const GrpProblem& q = a.p[p];
+    const int64_t nblk = (int64_t)q.tiles * q.nb;
+    if (grp_owner(a, q, nblk - 1) < w) continue;
+    // owner(i) >= w  <=>  (2 cost0 + (2 i + 1) c) W >= 2 w T
+    const int64_t cW = (int64_t)q.cost * a.workers;
+    const int64_t num = 2 * (int64_t)w * a.total_cost - 2 * q.cost0 * a.workers;
+    int64_t i = num > cW ? (num - cW + 2 * cW - 1) / (2 * cW) : 0;
+    if (i > nblk - 1) i = nblk - 1;
+    while (i > 0 && grp_owner(a, q, i - 1) >= w) --i;
+    while (grp_owner(a, q, i) < w) ++i;
+    p_out = p;
+    i_out = i;
+    g_out = q.blk0 + i;
+    return;
+  }
+  p_out = a.count;
+  i_out = 0;
+  g_out = a.total_blocks;
+}
+
+__device__ __forceinline__ void grp_store(const EpilogueArgs& e, int m, int n, uint32_t acc, int shift, int32_t ra,
+                                          int32_t rw, float wsc, float as) {
+  // acc = U * 2^shift; Y = U - h_w RA - h_a RW - Kpad h_a h_w (mod 2^32, exact: reading Q8)
+  const uint32_t y = (acc >> shift) - (uint32_t)e.h_w * (uint32_t)ra - (uint32_t)e.h_a * (uint32_t)rw -
+                     (uint32_t)e.kpad * (uint32_t)e.h_a * (uint32_t)e.h_w;
+  if (m >= e.M || n >= e.N) return;
+  const int64_t off = e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m;
+  if (e.kind == 2) {
+    const float v = ((float)(int32_t)y * wsc) * as;
+    unsigned short hv;
+    asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hv) : "f"(v));
+    reinterpret_cast<unsigned short*>(e.out)[off] = hv;
+  } else {
+    const uint32_t yb = 4u * y + 2u * (uint32_t)ra + 2u * (uint32_t)rw + (uint32_t)e.K;  // Y' (I2)
+    reinterpret_cast<int32_t*>(e.out)[off] = (int32_t)(e.kind == 1 ? yb : y);
+  }
+}
+
+// mbarrier phase wait: spin on try_wait (no suspend hint: the pipeline is short and a sleeping warp
+// wakes late), or with the hint under APT_GRP_SLEEP
+__device__ __forceinline__ void grp_wait(uint32_t bar, uint32_t parity) {
+#ifdef APT_GRP_SLEEP
+  mbar_wait(bar, parity);
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "GW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra GW_%=;\n}" ::"r"(bar), "r"(parity)
+      : "memory");
+#endif
+}
+
+template <int WBMAX, bool MT1>
+__global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant__ GrpArgs a) {
+  using SH = GrpShape<WBMAX>;
+  constexpr int D = SH::kD;
+  extern __shared__ __align__(1024) uint8_t smem[];  // no static shared memory: the swizzled token
+  // (the token boxes need 1024-byte alignment)
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = blockIdx.x;  // worker = CTA
+  const uint32_t sbase = smem_u32(smem);
+  auto full = [&](int s) { return sbase + (uint32_t)(SH::kBarOff + s * 8); };
+  auto empty = [&](int s) { return sbase + (uint32_t)(SH::kBarOff + (D + s) * 8); };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < D; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  int p0, p1;
+  int64_t i0, i1, gstart, gend;
+  grp_find(a, w, p0, i0, gstart);
+  grp_find(a, w + 1, p1, i1, gend);
+  (void)p1;
+  (void)i1;
+  if (gstart >= gend) return;
+
+  if (warp == 4) {
+    // ---- producer (one lane): per unit, WB bulk copies of 4 KB (weight planes) + M row copies of 256 B
+    // (token digits), completing on the slot's full barrier; the weights of the first D units are
+    // requested before griddepcontrol.wait (weights never depend on the previous kernel)
+    if (lane != 0) return;
+    // the current problem's fields live in registers (re-read from the parameter space only when the
+    // producer moves on to the next problem: indexed constant loads are slow)
+    int pp = p0, ptile = (int)(i0 / a.p[p0].nb), pblk = (int)(i0 - (int64_t)ptile * a.p[p0].nb);
+    int pnb, ptiles, pwb;
+    uint32_t ptx;
+    int64_t pps;
+    const uint32_t* pwp;
+    const CUtensorMap* ptok;
+    auto load_problem = [&]() {
+      const GrpProblem& q = a.p[pp];
+      pnb = q.nb;
+      ptiles = q.tiles;
+      pwb = q.wbits;
+      pps = q.w_pstride;
+      pwp = q.wp;
+      ptok = &q.tok;
+      ptx = (uint32_t)pwb * 4096u + (uint32_t)q.e.M * 256u;
+    };
+    load_problem();
+    auto weights = [&](int slot) {
+      mbar_expect_tx(full(slot), ptx);
+      const uint32_t* src = pwp + ((int64_t)ptile * pnb + pblk) * 1024;
+      for (int i = 0; i < pwb; ++i)
+        bulk_load(sbase + (uint32_t)(slot * SH::kSlot + i * 4096), src + i * pps, 4096u, full(slot));
+    };
+    auto tokens = [&](int slot) {
+      const uint32_t dst = sbase + (uint32_t)(slot * SH::kSlot + SH::kTok);
+      tma_load_2d(dst, ptok, full(slot), pblk * 256, 0);
+      tma_load_2d(dst + 2048, ptok, full(slot), pblk * 256 + 128, 0);
+    };
+    auto advance = [&]() {
+      if (++pblk == pnb) {
+        pblk = 0;
+        if (++ptile == ptiles) {
+          ptile = 0;
+          if (++pp < a.count) load_problem();
+        }
+      }
+    };
+    const int64_t U = gend - gstart;
+    const int pre = (int)min((int64_t)D, U);
+    {
+      const int qp = pp, qt = ptile, qb = pblk;
+      for (int u = 0; u < pre; ++u) {
+        weights(u);
+        advance();
+      }
+      pdl_wait();
+      pp = qp;
+      ptile = qt;
+      pblk = qb;
+      load_problem();
+      for (int u = 0; u < pre; ++u) {
+        tokens(u);
+        advance();
+      }
+    }
+    int slot = pre % D;
+    uint32_t ph = pre / D;  // completed passes over the ring
+    for (int64_t u = pre; u < U; ++u) {
+      grp_wait(empty(slot), (ph & 1) ^ 1);  // (the consumers fence their generic reads of the slot)
+      weights(slot);
+      tokens(slot);
+      advance();
+      if (++slot == D) {
+        slot = 0;
+        ++ph;
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: warp cw owns weight rows 32 cw .. 32 cw + 31 of each 128-row tile
+  pdl_wait();  // scales / row sums of the activations, the output and the workspace
+  const int cw = warp;
+  const int g = lane >> 2, t = lane & 3;
+  int cp = p0;
+  int64_t ci = i0, cg = gstart;
+  int slot = 0;
+  uint32_t ph = 0;
+#pragma unroll 1
+  while (cg < gend) {
+    const GrpProblem& q = a.p[cp];
+    const int nb = q.nb;
+    const int tile = (int)(ci / nb), b_in = (int)(ci - (int64_t)tile * nb);
+    const int seg = (int)min((int64_t)(nb - b_in), gend - cg);
+    const int n_w = tile * 128 + cw * 32;
+    const bool narrow = MT1 && q.e.M <= 8;
+    // lane (g, t) takes words t and t + 4 of every 256-element block (both operands, so K agrees):
+    // tokens: row r, 32-byte word t of box 0 / box 1 = 16-byte chunks 2t, 2t + 1 at chunk ^ (r & 7)
+    // (128-byte swizzle); weights: word t of half 0 / half 1 of row r = 4 bytes at h * 2048 + r * 16 + 4t.
+    // Every 8-lane (16-byte) / 32-lane (4-byte) shared-memory access is conflict-free.  Token rows >= M
+    // hold stale data; their products are never stored.
+    const uint32_t trow0 = (uint32_t)(SH::kTok + g * 128);
+    const uint32_t trow1 = trow0 + 8 * 128;
+    const uint32_t woff = (uint32_t)((cw * 32 + g) * 16 + t * 4);
+
+    int acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0;
+
+    auto run = [&](auto wbc, auto mtc) {
+      constexpr int WB = decltype(wbc)::value;
+      constexpr int MT = decltype(mtc)::value;
+#pragma unroll 1
+      for (int b = 0; b < seg; ++b) {
+        grp_wait(full(slot), ph & 1);
+        const uint32_t sl = sbase + (uint32_t)(slot * SH::kSlot);
+        uint4 tk0[4], tk1[4];  // [2 box + k]: word t (box 0) then word t + 4 (box 1), rows g / g + 8
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t ch = (uint32_t)((j >> 1) * 2048 + (((2 * t + (j & 1)) ^ g) * 16));  // (r & 7) == g
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(tk0[j].x), "=r"(tk0[j].y), "=r"(tk0[j].z), "=r"(tk0[j].w)
+                       : "r"(sl + trow0 + ch));
+          if (MT == 2)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(tk1[j].x), "=r"(tk1[j].y), "=r"(tk1[j].z), "=r"(tk1[j].w)
+                         : "r"(sl + trow1 + ch));
+        }
+        if constexpr (MT == 2) {
+          // weights = B operand (8 rows per MMA), tokens g, g + 8 = A operand: acc[4 qq + j]
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            uint2 wv[WB];  // .x = word t (half 0), .y = word t + 4 (half 1)
+#pragma unroll
+            for (int i = 0; i < WB; ++i) {
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wv[i].x) : "r"(sl + woff + (uint32_t)(i * 4096 + qq * 128)));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wv[i].y) : "r"(sl + woff + (uint32_t)(i * 4096 + 2048 + qq * 128)));
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              uint32_t wr[WB], o[8];
+#pragma unroll
+              for (int i = 0; i < WB; ++i) wr[i] = c ? wv[i].y : wv[i].x;
+              grp_rebuild<WB>(wr, o);
+              const uint32_t* ag = reinterpret_cast<const uint32_t*>(&tk0[2 * c]);
+              const uint32_t* ah = reinterpret_cast<const uint32_t*>(&tk1[2 * c]);
+#pragma unroll
+              for (int s4 = 0; s4 < 4; ++s4)
+                grp_mma(*reinterpret_cast<int(*)[4]>(acc + 4 * qq), ag[2 * s4], ah[2 * s4], ag[2 * s4 + 1], ah[2 * s4 + 1],
+                        o[2 * s4], o[2 * s4 + 1]);
+            }
+          }
+        } else {
+          // M <= 8: weights = A operand (rows g, g + 8 of each 16-row pair), tokens g = B operand: half the
+          // MMAs; acc[4 P + j]
+#pragma unroll
+          for (int P = 0; P < 2; ++P) {
+            uint2 wg[WB], wh[WB];
+#pragma unroll
+            for (int i = 0; i < WB; ++i) {
+              const uint32_t b = sl + woff + (uint32_t)(i * 4096 + P * 256);
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wg[i].x) : "r"(b));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wg[i].y) : "r"(b + 2048));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wh[i].x) : "r"(b + 128));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wh[i].y) : "r"(b + 2048 + 128));
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              uint32_t xg[WB], xh[WB], og[8], oh[8];
+#pragma unroll
+              for (int i = 0; i < WB; ++i) {
+                xg[i] = c ? wg[i].y : wg[i].x;
+                xh[i] = c ? wh[i].y : wh[i].x;
+              }
+              grp_rebuild<WB>(xg, og);
+              grp_rebuild<WB>(xh, oh);
+              const uint32_t* ag = reinterpret_cast<const uint32_t*>(&tk0[2 * c]);
+#pragma unroll
+              for (int s4 = 0; s4 < 4; ++s4)
+                grp_mma(*reinterpret_cast<int(*)[4]>(acc + 4 * P), og[2 * s4], oh[2 * s4], og[2 * s4 + 1], oh[2 * s4 + 1],
+                        ag[2 * s4], ag[2 * s4 + 1]);
+            }
+          }
+        }
+        // this warp is done with the slot: order its generic-proxy reads before the producer's next
+        // async-proxy (bulk copy / TMA) write of the slot, then release it.  The fence sits here, not in
+        // the producer: there it would also wait for the producer's own bulk copies in flight.
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty(slot));
+        if (++slot == D) {
+          slot = 0;
+          ++ph;
+        }
+      }
+      return 0;
+    };
+    auto run_w = [&](auto mtc) {
+      using std::integral_constant;
+      switch (q.wbits) {
+        case 1: return run(integral_constant<int, 1>{}, mtc);
+        case 2: return run(integral_constant<int, 2>{}, mtc);
+        case 3: if constexpr (WBMAX >= 3) return run(integral_constant<int, 3>{}, mtc); break;
+        case 4: if constexpr (WBMAX >= 4) return run(integral_constant<int, 4>{}, mtc); break;
+        case 5: if constexpr (WBMAX >= 5) return run(integral_constant<int, 5>{}, mtc); break;
+        case 6: if constexpr (WBMAX >= 6) return run(integral_constant<int, 6>{}, mtc); break;
+        case 7: if constexpr (WBMAX >= 7) return run(integral_constant<int, 7>{}, mtc); break;
+        default: if constexpr (WBMAX >= 8) return run(integral_constant<int, 8>{}, mtc); break;
+      }
+      return 0;
+    };
+    if (narrow) {
+      if constexpr (MT1) run_w(std::integral_constant<int, 1>{});
+    } else {
+      run_w(std::integral_constant<int, 2>{});
+    }
+    const int shift = grp_shift(q.wbits);
+
+    // ---- the tile: whole (one CTA) or split (partials + ticket; the last CTA to arrive reduces)
+    const int64_t tfirst = (int64_t)tile * nb;
+    const int fw = grp_owner(a, q, tfirst), lw = grp_owner(a, q, tfirst + nb - 1);
+    bool epi = true;
+    if (fw != lw) {
+      // each consumer warp reduces its own 32-row slice: partial, warp barrier (orders the lanes' stores
+      // before lane 0's ticket), acq_rel ticket at GPU scope (release: cumulative over those stores;
+      // acquire: the last arrival sees every other CTA's slice), warp barrier, reduction
+      int* part = a.partials + (((int64_t)w * 2 + (w == fw ? 1 : 0)) * 4 + cw) * 512;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) __stcg(part + j * 32 + lane, acc[j]);
+      __syncwarp();
+      unsigned prev = 0;
+      if (lane == 0) {
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.tickets + fw * 4 + cw) : "memory");
+        if (prev == (unsigned)(lw - fw))
+          asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a.tickets + fw * 4 + cw), "r"(0u) : "memory");
+      }
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      epi = prev == (unsigned)(lw - fw);
+      if (epi) {
+        __syncwarp();
+#pragma unroll 1
+        for (int o = fw; o <= lw; ++o) {
+          if (o == w) continue;
+          const int* po = a.partials + (((int64_t)o * 2 + (o == fw ? 1 : 0)) * 4 + cw) * 512;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] += __ldcg(po + j * 32 + lane);
+        }
+      }
+    }
+    if (epi) {
+      const EpilogueArgs& e = q.e;
+      const bool f16 = e.kind == 2;
+      if (!narrow) {  // acc[4 qq + 2 h + c]: token g + 8h, weight row n_w + 8 qq + 2t + c
+        int32_t ra[2];
+        float as[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int m = min(g + 8 * h, e.M - 1);
+          ra[h] = __ldg(e.a_rowsum + m);
+          as[h] = (f16 && e.a_scale) ? __ldg(e.a_scale + m) : 1.f;
+        }
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int n = n_w + 8 * qq + 2 * t + c, nc = min(n, e.N - 1);
+            const int32_t rw = __ldg(e.w_rowsum + nc);
+            const float wsc = f16 ? __ldg(e.w_scale + nc) : 0.f;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              grp_store(e, g + 8 * h, n, (uint32_t)acc[4 * qq + 2 * h + c], shift, ra[h], rw, wsc, as[h]);
+          }
+      } else {  // acc[4 P + 2 h + c]: weight row n_w + 16 P + g + 8 h, token 2t + c
+        int32_t ra[2];
+        float as[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int m = min(2 * t + c, e.M - 1);
+          ra[c] = __ldg(e.a_rowsum + m);
+          as[c] = (f16 && e.a_scale) ? __ldg(e.a_scale + m) : 1.f;
+        }
+#pragma unroll
+        for (int P = 0; P < 2; ++P)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int n = n_w + 16 * P + g + 8 * h, nc = min(n, e.N - 1);
+            const int32_t rw = __ldg(e.w_rowsum + nc);
+            const float wsc = f16 ? __ldg(e.w_scale + nc) : 0.f;
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              grp_store(e, 2 * t + c, n, (uint32_t)acc[4 * P + 2 * h + c], shift, ra[c], rw, wsc, as[c]);
+          }
+      }
+    }
+    ci += seg;
+    cg += seg;
+    if (ci == (int64_t)q.tiles * nb) {
+      ci = 0;
+      ++cp;
+    }
+  }
+}
+
+template <int WBMAX, bool MT1>
+static cudaError_t launch_grp2(const GrpArgs& a, int ctas, cudaStream_t stream) {
+  constexpr int kSmem = GrpShape<WBMAX>::kSmem;
+  cudaError_t err = set_smem_once<gemm_grp_kernel<WBMAX, MT1>>(kSmem);
+  if (err != cudaSuccess) return err;
+  return launch_pdl(gemm_grp_kernel<WBMAX, MT1>, dim3(ctas), dim3(160), kSmem, stream, dim3(1, 1, 1), a);
+}
+
+int grp_wbmax_class(int wbmax) { return wbmax <= 2 ? 2 : wbmax <= 4 ? 4 : 8; }
+// CTAs per SM (shared memory: 3 x 72 KB at WBMAX 2, 3 x 60 KB at WBMAX 4, 2 x 108 KB at WBMAX 8)
+int grp_ctas_per_sm(int wbmax) { return grp_wbmax_class(wbmax) <= 4 ? 3 : 2; }
+
+#ifndef APT_GRP_MT1
+#define APT_GRP_MT1 true
+#endif
+cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, cudaStream_t stream) {
+  switch (grp_wbmax_class(wbmax)) {
+    case 2: return launch_grp2<2, APT_GRP_MT1>(a, ctas, stream);
+    case 4: return launch_grp2<4, APT_GRP_MT1>(a, ctas, stream);
+    default: return launch_grp2<8, APT_GRP_MT1>(a, ctas, stream);
+  }
+}
+
+}  // namespace apt

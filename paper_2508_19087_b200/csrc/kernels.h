@@ -1,6 +1,7 @@
 // kernels.h — launch interfaces between the C-ABI shim (apt.cu) and the kernels.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -96,4 +97,31 @@ cudaError_t launch_zp_epilogue(const ZpArgs& p, cudaStream_t stream);
 // ablation (the paper's "Basic" recovery in global memory): out = sum_{i,j} 2^(i+j) parts[i * wbits + j]
 cudaError_t launch_recombine_planes(const int32_t* parts, int abits, int wbits, int64_t part_stride, int64_t count,
                                     int32_t* out, cudaStream_t stream);
+}  // namespace apt
+
+namespace apt {
+// grouped decode GEMM (gemm_grp.cu): up to kGrpMax independent problems (M <= 16, tile-major W, digit-
+// view A) in one persistent launch, stream-K over 32-row x 256-K blocks; passed by value (kernel
+// parameter space, so a CUDA graph captures the whole group)
+constexpr int kGrpMax = 64;
+struct GrpProblem {
+  CUtensorMap tok;         // activation digit view [M][Kpad] u8, 128 x 16 boxes, 128-byte swizzle
+  const uint32_t* wp;      // tile-major weight planes
+  int64_t w_pstride;       // words per plane
+  const uint8_t* adig;     // activation digits [M][Kpad], kernel K order
+  EpilogueArgs e;
+  int64_t blk0;            // global index of the problem's first block (tile-major, then K)
+  int64_t cost0;           // total cost of the blocks before the problem
+  int32_t k_words, nb, tiles, wbits, cost;  // nb = Kpad / 256 blocks per row tile; tiles = ceil(N / 128)
+};
+struct GrpArgs {
+  int32_t count, workers;  // workers = warps of the grid; workers * max cost <= total_cost
+  int64_t total_blocks, total_cost;
+  int32_t* partials;       // [workers][2][16 x 32] int32
+  uint32_t* tickets;       // [workers], zero before and after the call
+  GrpProblem p[kGrpMax];
+};
+int grp_wbmax_class(int wbmax);
+int grp_ctas_per_sm(int wbmax);
+cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, cudaStream_t stream);
 }  // namespace apt

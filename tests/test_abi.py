@@ -25,7 +25,7 @@ def test_header_symbols_exported():
     lib = L.lib()
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.apt_abi_version() == L.ABI_VERSION == 4
+    assert lib.apt_abi_version() == L.ABI_VERSION == 5
 
 
 def test_status_strings():
@@ -186,3 +186,15 @@ def test_python_api_refuses_cpu_tensors():
     import paper_2508_19087_b200 as P
     with pytest.raises(ValueError):
         P.pack(torch.zeros((2, 2), dtype=torch.int8), 2)
+
+
+def test_grouped_argument_errors_without_gpu():
+    """apt_gemm_grouped rejects a bad group size / null array before touching the device."""
+    lib = L.lib()
+    assert lib.apt_gemm_grouped(0, None, None, 0, None) == L.APT_ERR_INVALID_ARGUMENT
+    assert lib.apt_gemm_grouped(L.APT_GROUP_MAX + 1, None, None, 0, None) == L.APT_ERR_INVALID_ARGUMENT
+    arr = (L.AptGemmProblem * 1)()
+    arr[0].M = 17  # more tokens than the decode kernel's 16
+    assert lib.apt_gemm_grouped(1, arr, None, 0, None) == L.APT_ERR_INVALID_ARGUMENT
+    assert lib.apt_gemm_grouped_workspace_bytes(0) == 0
+    assert lib.apt_gemm_grouped_workspace_bytes(1) >= 16384 + 148 * 3 * 2 * 4 * 512 * 4

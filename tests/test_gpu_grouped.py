@@ -1,0 +1,173 @@
+"""GPU parity of the grouped decode GEMM (apt_gemm_grouped, gemm_grp.cu) against the CPU oracle.
+
+Each problem of a group must equal the oracle exactly like a single apt_gemm call (int32 bit-exact,
+fp16 within 1e-3 of the fp64-scaled oracle), whatever the group around it: the
+stream-K schedule splits row tiles between warps at arbitrary K blocks and across problem boundaries.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import apt_oracle as O
+from oracle import c_gemm_i64
+from synth import config_seed, log_uniform_scales, signed_codes
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2508_19087_b200")
+
+DEV = "cuda:0"
+TOL = 1e-3
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _problem(m, n, k, pw, pa, seed, kind="i32", layout="row"):
+    a = signed_codes(m, k, pa, seed=seed)
+    w = signed_codes(n, k, pw, seed=seed + 1)
+    ws = log_uniform_scales(n, -10, -6, seed=seed + 2)
+    as_ = log_uniform_scales(m, -6, -2, seed=seed + 3)
+    pr = dict(W=P.pack(_dev(w), pw, tiled=True), A=P.pack(_dev(a), pa, digits=True), out_kind=kind, layout=layout)
+    if kind == "f16":
+        pr.update(w_scale=_dev(ws), a_scale=_dev(as_))
+    return pr, (a, w, ws, as_, pw, pa)
+
+
+def _check(out, kind, layout, a, w, ws, as_, pw, pa, exact_ref=None):
+    got = out.cpu().numpy()
+    if layout == "col":
+        got = got.T
+    ref = exact_ref if exact_ref is not None else O.gemm_signed(a, w)
+    if kind == "i32":
+        assert np.array_equal(got.astype(np.int64), ref)
+    elif kind == "bipolar":
+        assert np.array_equal(got.astype(np.int64), O.gemm_bipolar(a, pa, w, pw))
+    else:
+        r = O.scale_fp64(ref, ws, as_)
+        assert (np.abs(got.astype(np.float64) - r) <= TOL * np.abs(r) + 2.0 ** -24).all()
+
+
+def _tickets_zero():
+    torch.cuda.synchronize()
+    ws = P.grouped_workspace(DEV)
+    assert int(ws[:16384].count_nonzero().item()) == 0
+
+
+RAGGED = [  # (m, n, k, pw, pa): N not a multiple of 32 / 128, K not a multiple of 256, tiny and long K
+    (1, 333, 700, 1, 2), (3, 100, 64, 2, 2), (8, 41, 1300, 3, 4), (9, 256, 4096, 4, 4), (16, 300, 4096, 2, 8),
+    (16, 1, 1, 1, 1), (5, 77, 2600, 4, 3), (2, 129, 513, 1, 8), (12, 64, 9000, 3, 2), (16, 40, 256, 4, 4),
+]
+
+
+@pytest.mark.parametrize("kind,layout", [("i32", "row"), ("bipolar", "col"), ("f16", "row"), ("f16", "col")])
+def test_grouped_ragged_mixed(kind, layout):
+    """Ten ragged problems of mixed width / token count in one launch."""
+    prs, refs = zip(*[_problem(m, n, k, pw, pa, 500 + 7 * i, kind, layout) for i, (m, n, k, pw, pa) in enumerate(RAGGED)])
+    outs = P.gemm_grouped(prs)
+    for out, ref in zip(outs, refs):
+        _check(out, kind, layout, *ref)
+    _tickets_zero()
+
+
+@pytest.mark.parametrize("wmax", [2, 4, 8])
+@pytest.mark.parametrize("count", [1, 2, 7, 64])
+def test_grouped_counts_and_width_classes(wmax, count):
+    """1..64 problems (APT_GROUP_MAX), every kernel width class (WBMAX 2 / 4 / 8 rings)."""
+    rng = np.random.default_rng(wmax * 100 + count)
+    cases = []
+    for i in range(count):
+        m = int(rng.integers(1, 17))
+        n = int(rng.integers(1, 400))
+        k = int(rng.integers(1, 3000))
+        pw = int(rng.integers(1, wmax + 1)) if i else wmax
+        pa = int(rng.integers(1, 9))
+        cases.append((m, n, k, pw, pa))
+    prs, refs = zip(*[_problem(*c, seed=900 + 11 * i) for i, c in enumerate(cases)])
+    outs = P.gemm_grouped(prs)
+    for out, ref in zip(outs, refs):
+        _check(out, "i32", "row", *ref)
+    _tickets_zero()
+
+
+def test_grouped_equals_apt_gemm_bitwise():
+    """Same bits as the per-call apt_gemm (int32 and fp16) on decode-shaped problems."""
+    cases = [(1, 4096, 4096, 1, 2), (8, 4096, 11008, 2, 2), (16, 11008, 4096, 4, 4), (16, 4096, 4096, 3, 4)]
+    for kind in ("i32", "f16"):
+        prs = [_problem(*c, seed=40 + i, kind=kind)[0] for i, c in enumerate(cases)]
+        outs = P.gemm_grouped(prs)
+        for pr, out in zip(prs, outs):
+            one = P.gemm(pr["W"], pr["A"], out_kind=kind, w_scale=pr.get("w_scale"), a_scale=pr.get("a_scale"))
+            assert torch.equal(one.view(torch.int16) if kind == "f16" else one,
+                               out.view(torch.int16) if kind == "f16" else out)
+
+
+LLAMA7B = [(4096, 4096), (11008, 4096), (4096, 11008)]
+PRECISIONS = [(1, 2), (2, 2), (3, 4), (4, 4)]
+
+
+@pytest.mark.parametrize("by_precision", [False, True])
+def test_grouped_llama7b_decode_full(by_precision):
+    """BASELINE configs[1] exactly as bench.py times the grouped leg: the 36 decode linears (fp16,
+    per-channel w_scale, per-token a_scale) in one launch, or one launch per precision; every output
+    element within 1e-3 of the fp64-scaled C int64 oracle."""
+    groups = [[pq] for pq in PRECISIONS] if by_precision else [PRECISIONS]
+    for precs in groups:
+        prs, refs = [], []
+        for (pw, pa) in precs:
+            for (n, k) in LLAMA7B:
+                for m in (1, 8, 16):
+                    seed = config_seed(1, pw, pa, salt=13) + n + m
+                    pr, ref = _problem(m, n, k, pw, pa, seed, kind="f16")
+                    prs.append(pr)
+                    refs.append(ref)
+        outs = P.gemm_grouped(prs)
+        for out, (a, w, ws, as_, pw, pa) in zip(outs, refs):
+            _check(out, "f16", "row", a, w, ws, as_, pw, pa, exact_ref=c_gemm_i64(a, w))
+    _tickets_zero()
+
+
+def test_grouped_repeat_and_repack_stream_order():
+    """50 back-to-back grouped calls on one stream, with the activations re-packed (different codes into
+    the same buffers) right before every call: each call sees its own codes."""
+    cases = [(16, 4096, 4096, 2, 2), (8, 11008, 4096, 4, 4), (1, 4096, 11008, 1, 2)]
+    prs = [_problem(*c, seed=70 + i)[0] for i, c in enumerate(cases)]
+    for it in range(50):
+        refs = []
+        for (m, n, k, pw, pa), pr, i in zip(cases, prs, range(3)):
+            a = signed_codes(m, k, pa, seed=10000 + 3 * it + i)
+            P.pack(_dev(a), pa, out=pr["A"])
+            refs.append(a)
+        outs = P.gemm_grouped(prs)
+        if it % 10 == 9:
+            for out, a, pr, (m, n, k, pw, pa) in zip(outs, refs, prs, cases):
+                w = signed_codes(n, k, pw, seed=70 + cases.index((m, n, k, pw, pa)) + 1)
+                assert np.array_equal(out.cpu().numpy().astype(np.int64), c_gemm_i64(a, w))
+    _tickets_zero()
+
+
+def test_grouped_extremes():
+    """All-extreme codes at the largest K the unsigned digit sum allows (Kpad * 255 * 255 < 2^32)."""
+    k = 66048
+    prs, exp = [], []
+    for av, wv, pw in ((-128, -2, 2), (127, 1, 2), (-128, 7, 4), (-1, -1, 1)):
+        a = np.full((16, k), av, dtype=np.int8)
+        w = np.full((40, k), wv, dtype=np.int8)
+        prs.append(dict(W=P.pack(_dev(w), pw, tiled=True), A=P.pack(_dev(a), 8, digits=True)))
+        exp.append(np.full((16, 40), k * av * wv, dtype=np.int64))
+    for out, e in zip(P.gemm_grouped(prs), exp):
+        assert np.array_equal(out.cpu().numpy().astype(np.int64), e)
+
+
+def test_grouped_rejects():
+    """Argument errors come back before any launch."""
+    pr, _ = _problem(4, 64, 256, 2, 2, seed=3)
+    bad_rows = dict(pr, W=P.pack(_dev(signed_codes(64, 256, 2, seed=4)), 2))  # canonical (row) layout
+    bad_dig = dict(pr, A=P.pack(_dev(signed_codes(4, 256, 2, seed=5)), 2))     # no digit view
+    bad_m = dict(pr, A=P.pack(_dev(signed_codes(17, 256, 2, seed=6)), 2, digits=True))
+    for bad in (bad_rows, bad_dig, bad_m):
+        with pytest.raises(P._lib.AptError):
+            P.gemm_grouped([pr, bad])
+    with pytest.raises(ValueError):
+        P.gemm_grouped([pr] * 65)
