@@ -4,9 +4,13 @@
 Default workload (BASELINE.json configs[1], "llama2-7b-decode"): one STEP is the whole per-call
 hot path for every Llama-2-7B decode linear (N x K = 4096x4096, 11008x4096, 4096x11008) at
 M = 1, 8, 16 tokens and W1A2, W2A2, W3A4, W4A4 (36 cases): the 12 distinct activations packed
-(apt_pack_bipolar), then the 36 bit-plane GEMMs with the fused fp16 scale epilogue (apt_gemm).  Weight packing is offline (done
-once, timed separately and reported as `weight_pack`).  Two packed-weight sets (2 x 133 MB > L2)
-alternate between steps so weights stream from HBM.  Steps are replayed as CUDA graphs.
+(apt_pack_bipolar), then the 36 bit-plane GEMMs with the fused fp16 scale epilogue.  The 36 GEMMs are
+independent problems; by default (--decode grouped) they run through apt_gemm_grouped, one persistent
+launch per precision (9 problems each), every problem with its OWN packed weights (3 copies per linear,
+so no problem reads another's weights from L2); --decode per_call runs 36 apt_gemm launches instead (the
+per-GEMM path, also reported under `per_call` in the default run).  Weight packing is offline (done once,
+timed separately and reported as `weight_pack`).  Two packed-weight sets (2 x 400 MB grouped, 2 x 133 MB
+per-call, both > L2) alternate between steps so weights stream from HBM.  Steps are replayed as CUDA graphs.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl apt|reference]
 
@@ -49,10 +53,12 @@ def log(msg):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="apt", choices=["apt", "reference"])
     ap.add_argument("--no-baselines", action="store_true", help="skip cuBLAS / oracle / e2e legs")
+    ap.add_argument("--decode", default="grouped", choices=["grouped", "per_call"],
+                    help="decode GEMM phase: apt_gemm_grouped (one launch per precision) or 36 apt_gemm launches")
     ap.add_argument("--legs", default="all",
                     help="extra BASELINE configs timed in the same run: all | none | comma list of prefill,llama70b,sweep")
     return ap.parse_args()
@@ -80,9 +86,9 @@ def kernel_mix(cfgs):
     return mix
 
 
-def load_traffic():
+def load_traffic(name="decode_traffic.json"):
     try:
-        with open(os.path.join(ROOT, "profiles", "decode_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             return json.load(f)
     except Exception:
         return None
@@ -274,6 +280,11 @@ def main():
     wpack_ms = e0.elapsed_time(e1)
     wpack_bytes = sum(c.numel() + P.kpad(c.shape[1]) * c.shape[0] * wb // 8 for (s, wb, n, k), c in W_codes.items())
     del W_codes
+    # grouped path: every problem has its own packed weights (the M = 1, 8, 16 problems of one launch never
+    # share a weight buffer, so no problem's weights are served from L2 by another's reads), 2 sets
+    W_grp = [[P.pack(codes(shard[n], k, wb), wb, tiled=True) for (m, wb, ab, n, k) in CASES] for _ in range(2)]
+    PREC_IDX = [[i for i, c in enumerate(CASES) if (c[1], c[2]) == pq] for pq in PRECISIONS]
+    ws_grp = P.grouped_workspace(dev)
 
     # one step = pack every distinct activation (m, abits, K) once (12 packs; the 4096x4096 and 11008x4096
     # linears of a precision share their input), then the 36 GEMMs (+ the all-gather of each output at N>1)
@@ -281,12 +292,31 @@ def main():
         for key in A_codes:
             P.pack(A_codes[key], key[1], out=A_buf[key])
 
-    def gemm_step(wset):
+    def decode_gemms(mode, wset, a_of, scale_of, out_of, gather=True, groups=None):
+        """The 36 decode GEMMs of one step: apt_gemm_grouped per precision (mode "grouped"; `groups` overrides
+        which problems share a launch) or one apt_gemm per case (mode "per_call"); at N > 1 each output slice
+        is all-gathered."""
+        if mode == "grouped":
+            for idx in (PREC_IDX if groups is None else groups):
+                P.gemm_grouped([dict(W=W_grp[wset][i], A=a_of(i), out_kind="f16", layout=layout,
+                                     w_scale=W_scale[CASES[i][1:2] + CASES[i][3:]], a_scale=scale_of(i),
+                                     out=out_of(i)) for i in idx], workspace=ws_grp, stream=stream)
+                if world > 1 and gather:
+                    for i in idx:
+                        dist.all_gather_into_tensor(gathered[i], out_of(i))
+            return
         for i, (m, wb, ab, n, k) in enumerate(CASES):
-            P.gemm(W_packed[wset][(wb, n, k)], A_buf[(m, ab, k)], out_kind="f16", layout=layout,
-                   w_scale=W_scale[(wb, n, k)], a_scale=A_scale[m], out=outs[i], config=cfgs[i])
-            if world > 1:
-                dist.all_gather_into_tensor(gathered[i], outs[i])
+            P.gemm(W_packed[wset][(wb, n, k)], a_of(i), out_kind="f16", layout=layout,
+                   w_scale=W_scale[(wb, n, k)], a_scale=scale_of(i), out=out_of(i), config=cfgs[i])
+            if world > 1 and gather:
+                dist.all_gather_into_tensor(gathered[i], out_of(i))
+
+    a_main = lambda i: A_buf[(CASES[i][0], CASES[i][2], CASES[i][4])]  # noqa: E731
+    s_main = lambda i: A_scale[CASES[i][0]]  # noqa: E731
+    o_main = lambda i: outs[i]  # noqa: E731
+
+    def gemm_step(wset, mode=args.decode):
+        decode_gemms(mode, wset, a_main, s_main, o_main)
 
     log("eager warm steps")
     for j in range(2):
@@ -311,6 +341,20 @@ def main():
         g_pack = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_pack, stream=stream):
             pack_step()
+        # the other decode path (per-call apt_gemm launches when the headline is grouped), reported beside it
+        g_step_pc, g_gemm_pc = [], []
+        if args.decode == "grouped":
+            for j in range(2):
+                gemm_step(j, "per_call")
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    pack_step()
+                    gemm_step(j, "per_call")
+                g_step_pc.append(gr)
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    gemm_step(j, "per_call")
+                g_gemm_pc.append(gr)
     except Exception as exc:  # NCCL capture unsupported -> eager launches (still every kernel ours)
         use_graphs = False
         print(f"[bench] graph capture failed ({exc!r}); timing eager steps", file=sys.stderr)
@@ -360,9 +404,38 @@ def main():
     bytes_all = sum(alg_bytes(m, shard[n], k, wb, ab) for (m, wb, ab, n, k) in CASES)
     hbm_peak, peak_src = load_peaks()
     achieved = bytes_all / (gemm_ms * 1e-3) / 1e9
-    traffic = load_traffic()
-    per_prec, per_m, per_kernel = breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, shard, layout,
-                                use_graphs, hbm_peak)
+    grouped = args.decode == "grouped"
+    traffic = load_traffic("grouped_traffic.json" if grouped else "decode_traffic.json")
+    per_prec_pc, per_m_pc, per_kernel = breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, shard,
+                                                  layout, use_graphs, hbm_peak)
+    if grouped:
+        per_prec, per_m = grouped_breakdown(torch, stream, decode_gemms, PREC_IDX, a_main, s_main, o_main, shard,
+                                            use_graphs, hbm_peak)
+        per_call = {"path": "36 apt_gemm launches per step (selector / autotuned-table configs), the per-call weights "
+                            "(2 sets x 133 MB; the M = 1, 8, 16 cases of a linear share a buffer)"}
+        if use_graphs:
+            for j in range(args.warmup):
+                g_step_pc[j % 2].replay()
+            barrier()
+            e0.record(stream)
+            for j in range(args.steps):
+                g_step_pc[j % 2].replay()
+            e1.record(stream)
+            barrier()
+            ms_pc = e0.elapsed_time(e1) / args.steps
+            gemm_ms_pc = phase_ms(lambda j: g_gemm_pc[j % 2].replay(), reps)
+            ach_pc = bytes_all / (gemm_ms_pc * 1e-3) / 1e9
+            per_call.update({"value": round(sum(2 * m * n * k for (m, wb, ab, n, k) in CASES) / (ms_pc * 1e-3) / 1e12, 4),
+                             "unit": "TOPS", "ms_per_step": round(ms_pc, 5),
+                             "gemm_us_per_step": round(1e3 * gemm_ms_pc, 2),
+                             "roofline": {"bound": "hbm", "achieved": round(ach_pc, 1), "peak": hbm_peak, "unit": "GB/s",
+                                          "frac": round(ach_pc / hbm_peak, 4),
+                                          "traffic": (load_traffic() or {}).get("dram_bytes_per_launch_avg"),
+                                          "kernel": ", ".join(f"{k} x{v}" for k, v in sorted(kernel_mix(cfgs).items())),
+                                          "gemm_us_per_launch": round(1e3 * gemm_ms_pc / len(CASES), 3)}})
+        per_call.update({"per_precision": per_prec_pc, "per_m": per_m_pc, "per_kernel": per_kernel})
+    else:
+        per_prec, per_m, per_call = per_prec_pc, per_m_pc, None
     line = {"metric": METRIC, "value": round(value, 4), "unit": "TOPS",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -370,23 +443,31 @@ def main():
             "config": {"workload": "llama2-7b-decode", "linears_NxK": SHAPES, "M": MS,
                        "precisions": [f"W{wb}A{ab}" for wb, ab in PRECISIONS], "cases_per_step": len(CASES),
                        "out": "fp16 scaled (w_scale[n], a_scale[m])",
-                       "l2": "inputs larger than L2: 2 alternating packed-weight sets (2 x 133 MB)",
+                       "l2": ("inputs larger than L2: 2 alternating packed-weight sets (2 x 400 MB, every problem its "
+                              "own weights)") if args.decode == "grouped" else
+                             "inputs larger than L2: 2 alternating packed-weight sets (2 x 133 MB)",
                        "parallelism": f"tp{world} (N-split + all-gather)" if world > 1 else "single GPU",
                        "cuda_graphs": use_graphs},
-            "gpu_launches": (len(A_codes) + len(CASES)) * args.steps,
-            "roofline": {"bound": "hbm", "kernel": "decode GEMM phase: " + ", ".join(
-                             f"{k} x{v}" for k, v in sorted(kernel_mix(cfgs).items())) + " launches/step",
+            "gpu_launches": (len(A_codes) + (len(PREC_IDX) if grouped else len(CASES))) * args.steps,
+            "decode_path": ("apt_gemm_grouped: one persistent launch per precision (9 independent problems each, "
+                            "every problem its own packed weights)") if grouped else "36 apt_gemm launches",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("gemm_grp_kernel (apt_gemm_grouped) x4 launches/step" if grouped else
+                                    "decode GEMM phase: " + ", ".join(
+                                        f"{k} x{v}" for k, v in sorted(kernel_mix(cfgs).items())) + " launches/step"),
                          "measured": "GEMM phase replayed alone right after the timed region (events around the graph "
-                                     "of 36 GEMM launches" + (" + all-gathers" if world > 1 else "") +
+                                     "of the step's GEMM launches" + (" + all-gathers" if world > 1 else "") +
                                      ", the two weight sets alternating)",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4),
                          "traffic": traffic.get("dram_bytes_per_launch_avg") if traffic else None,
-                         "alg_bytes_per_launch_avg": round(bytes_all / len(CASES)),
+                         "traffic_source": (traffic or {}).get("source"),
+                         "alg_bytes_per_launch_avg": round(bytes_all / (len(PREC_IDX) if grouped else len(CASES))),
                          "gemm_share_of_step": round(gemm_ms / ms_per_step, 3),
-                         "gemm_us_per_launch": round(1e3 * gemm_ms / len(CASES), 3)},
+                         "gemm_us_per_launch": round(1e3 * gemm_ms / (len(PREC_IDX) if grouped else len(CASES)), 3)},
             "act_pack": {"launches_per_step": len(A_codes), "us_per_step": round(1e3 * pack_ms, 3)},
-            "per_precision": per_prec, "per_m": per_m, "per_kernel": per_kernel,
+            "per_precision": per_prec, "per_m": per_m,
+            **({"per_call": per_call} if grouped else {"per_kernel": per_kernel}),
             "weight_pack": {"ms": round(wpack_ms, 3), "GB/s": round(wpack_bytes / (wpack_ms * 1e-3) / 1e9, 1)}}
 
     legs = {"prefill", "llama70b", "sweep"} if args.legs == "all" else set() if args.legs == "none" else \
@@ -397,7 +478,7 @@ def main():
     log("baselines")
     if not args.no_baselines:
         line.update(baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout,
-                              value, barrier))
+                              value, barrier, decode_gemms))
     clocks = sampler.summary(t_start, t_end)
     sampler.stop()
     line["clocks"] = clocks
@@ -638,7 +719,51 @@ def breakdown(torch, P, stream, W_packed, A_buf, W_scale, A_scale, outs, cfgs, s
     return per_prec, per_m, per_kernel
 
 
-def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout, value, barrier):
+def grouped_breakdown(torch, stream, decode_gemms, prec_idx, a_of, s_of, o_of, shard, use_graphs, hbm_peak):
+    """Grouped path per precision (its own single apt_gemm_grouped launch of 9 problems) and per M (one launch
+    of that M's 12 problems, mixed widths): graph replays with a 256 MB write between them, events around each."""
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=stream.device)
+    import paper_2508_19087_b200 as P
+
+    def stats(idx, decode_one):
+        gs = []
+        for wset in range(2):
+            fn = (lambda w=wset: decode_one(w))
+            fn()
+            if use_graphs:
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    fn()
+                gs.append(gr.replay)
+            else:
+                gs.append(fn)
+        ts = []
+        for r in range(20):
+            flush.fill_(r & 255)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            gs[r % 2]()
+            b.record(stream)
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        ms = statistics.median(x.elapsed_time(y) for x, y in ts)
+        ops = sum(2 * CASES[i][0] * shard[CASES[i][3]] * CASES[i][4] for i in idx)
+        byt = sum(alg_bytes(CASES[i][0], shard[CASES[i][3]], CASES[i][4], CASES[i][1], CASES[i][2]) for i in idx)
+        return {"launch_us": round(1e3 * ms, 2), "problems": len(idx), "eff_tops": round(ops / (ms * 1e-3) / 1e12, 3),
+                "hbm_frac": round(byt / (ms * 1e-3) / 1e9 / hbm_peak, 4)}
+
+    def one_launch(idx):
+        return lambda wset: decode_gemms("grouped", wset, a_of, s_of, o_of, gather=False, groups=[idx])
+
+    per_prec = {f"W{wb}A{ab}": stats(idx, one_launch(idx)) for (wb, ab), idx in zip(PRECISIONS, prec_idx)}
+    per_m = {f"M{m}": stats([i for i, c in enumerate(CASES) if c[0] == m],
+                            one_launch([i for i, c in enumerate(CASES) if c[0] == m])) for m in MS}
+    del flush
+    return per_prec, per_m
+
+
+def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout, value, barrier,
+              decode_gemms):
     """e2e through the public API with host buffers; cuBLAS FP16 / INT8 on the same cases; the CPU
     oracle on a bounded sample (rank 0, N=1)."""
     import torch
@@ -687,10 +812,9 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
                     P.quantize_pack(d_a[key], key[1], out=bufs[key], scale=q_scale[key])
                 else:
                     P.pack(d_a[key], key[1], out=bufs[key])
-            for i, (m, wb, ab, n, k) in enumerate(CASES):
-                P.gemm(W_packed[wset][(wb, n, k)], bufs[(m, ab, k)], out_kind="f16", layout=layout,
-                       w_scale=W_scale[(wb, n, k)], a_scale=q_scale[(m, ab, k)] if fp16 else A_scale[m],
-                       out=d_out[i], config=cfgs[i])
+            decode_gemms(args.decode, wset, lambda i: bufs[(CASES[i][0], CASES[i][2], CASES[i][4])],
+                         lambda i: q_scale[(CASES[i][0], CASES[i][2], CASES[i][4])] if fp16 else A_scale[CASES[i][0]],
+                         lambda i: d_out[i], gather=False)
             h_out_all.copy_(d_out_all, non_blocking=True)
 
         n_e2e = max(2, min(args.steps, 50))
@@ -714,8 +838,9 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
         s1.record()
         barrier()
         e2e_ms = s0.elapsed_time(s1) / n_e2e
-        path = ("pinned host fp16 activations -> 1 H2D -> 12x apt_quantize_pack -> 36x apt_gemm (fp16) -> 1 D2H"
-                if fp16 else "pinned host int8 codes -> 1 H2D -> 12x apt_pack_bipolar -> 36x apt_gemm (fp16) -> 1 D2H")
+        gm = "4x apt_gemm_grouped (36 GEMMs, fp16)" if args.decode == "grouped" else "36x apt_gemm (fp16)"
+        path = (f"pinned host fp16 activations -> 1 H2D -> 12x apt_quantize_pack -> {gm} -> 1 D2H"
+                if fp16 else f"pinned host int8 codes -> 1 H2D -> 12x apt_pack_bipolar -> {gm} -> 1 D2H")
         return {"value": round(ops_step / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TOPS",
                 "h2d_bytes_per_step": h_in.numel() * h_in.element_size(), "d2h_bytes_per_step": o_total * 2,
                 "ms_per_step": round(e2e_ms, 5), "steps": n_e2e, "path": path + ", CUDA graph"}
@@ -754,10 +879,9 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
                         P.quantize_pack(d_a[key], key[1], out=bufs[key], scale=q_scale[key])
                     else:
                         P.pack(d_a[key], key[1], out=bufs[key])
-                for i, (m, wb, ab, n, k) in enumerate(CASES):
-                    P.gemm(W_packed[b][(wb, n, k)], bufs[(m, ab, k)], out_kind="f16", layout=layout,
-                           w_scale=W_scale[(wb, n, k)], a_scale=q_scale[(m, ab, k)] if fp16 else A_scale[m],
-                           out=outs_b[i], config=cfgs[i])
+                decode_gemms(args.decode, b, lambda i: bufs[(CASES[i][0], CASES[i][2], CASES[i][4])],
+                             lambda i: q_scale[(CASES[i][0], CASES[i][2], CASES[i][4])] if fp16 else A_scale[CASES[i][0]],
+                             lambda i: outs_b[i], gather=False)
             comp()
             torch.cuda.synchronize()
             gr = torch.cuda.CUDAGraph()
@@ -803,8 +927,9 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
         torch.cuda.synchronize()
         barrier()
         e2e_ms = s0.elapsed_time(s1) / n_e2e
-        path = ("pinned host fp16 activations -> H2D -> 12x apt_quantize_pack -> 36x apt_gemm (fp16) -> D2H" if fp16
-                else "pinned host int8 codes -> H2D -> 12x apt_pack_bipolar -> 36x apt_gemm (fp16) -> D2H")
+        gm = "4x apt_gemm_grouped (36 GEMMs, fp16)" if args.decode == "grouped" else "36x apt_gemm (fp16)"
+        path = (f"pinned host fp16 activations -> H2D -> 12x apt_quantize_pack -> {gm} -> D2H" if fp16
+                else f"pinned host int8 codes -> H2D -> 12x apt_pack_bipolar -> {gm} -> D2H")
         return {"value": round(ops_step / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TOPS",
                 "h2d_bytes_per_step": off * (2 if fp16 else 1), "d2h_bytes_per_step": o_total * 2,
                 "ms_per_step": round(e2e_ms, 5), "steps": n_e2e,
