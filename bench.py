@@ -288,7 +288,12 @@ def main():
 
     # one step = pack every distinct activation (m, abits, K) once (12 packs; the 4096x4096 and 11008x4096
     # linears of a precision share their input), then the 36 GEMMs (+ the all-gather of each output at N>1)
-    def pack_step():
+    pack_problems = [dict(codes=A_codes[key], bits=key[1], out=A_buf[key]) for key in A_codes]
+
+    def pack_step(mode=args.decode):
+        if mode == "grouped":  # the 12 independent activation packs in one launch (apt_pack_grouped)
+            P.pack_grouped(pack_problems, stream=stream)
+            return
         for key in A_codes:
             P.pack(A_codes[key], key[1], out=A_buf[key])
 
@@ -348,7 +353,7 @@ def main():
                 gemm_step(j, "per_call")
                 gr = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gr, stream=stream):
-                    pack_step()
+                    pack_step("per_call")
                     gemm_step(j, "per_call")
                 g_step_pc.append(gr)
                 gr = torch.cuda.CUDAGraph()
@@ -411,8 +416,8 @@ def main():
     if grouped:
         per_prec, per_m = grouped_breakdown(torch, stream, decode_gemms, PREC_IDX, a_main, s_main, o_main, shard,
                                             use_graphs, hbm_peak)
-        per_call = {"path": "36 apt_gemm launches per step (selector / autotuned-table configs), the per-call weights "
-                            "(2 sets x 133 MB; the M = 1, 8, 16 cases of a linear share a buffer)"}
+        per_call = {"path": "12 apt_pack_bipolar + 36 apt_gemm launches per step (selector / autotuned-table configs), "
+                            "the per-call weights (2 sets x 133 MB; the M = 1, 8, 16 cases of a linear share a buffer)"}
         if use_graphs:
             for j in range(args.warmup):
                 g_step_pc[j % 2].replay()
@@ -448,7 +453,7 @@ def main():
                              "inputs larger than L2: 2 alternating packed-weight sets (2 x 133 MB)",
                        "parallelism": f"tp{world} (N-split + all-gather)" if world > 1 else "single GPU",
                        "cuda_graphs": use_graphs},
-            "gpu_launches": (len(A_codes) + (len(PREC_IDX) if grouped else len(CASES))) * args.steps,
+            "gpu_launches": ((1 + len(PREC_IDX)) if grouped else (len(A_codes) + len(CASES))) * args.steps,
             "decode_path": ("apt_gemm_grouped: one persistent launch per precision (9 independent problems each, "
                             "every problem its own packed weights)") if grouped else "36 apt_gemm launches",
             "roofline": {"bound": "hbm",
@@ -465,7 +470,9 @@ def main():
                          "alg_bytes_per_launch_avg": round(bytes_all / (len(PREC_IDX) if grouped else len(CASES))),
                          "gemm_share_of_step": round(gemm_ms / ms_per_step, 3),
                          "gemm_us_per_launch": round(1e3 * gemm_ms / (len(PREC_IDX) if grouped else len(CASES)), 3)},
-            "act_pack": {"launches_per_step": len(A_codes), "us_per_step": round(1e3 * pack_ms, 3)},
+            "act_pack": {"launches_per_step": 1 if grouped else len(A_codes), "packs_per_step": len(A_codes),
+                         "us_per_step": round(1e3 * pack_ms, 3),
+                         "path": "apt_pack_grouped (12 packs, one launch)" if grouped else "12 apt_pack_bipolar"},
             "per_precision": per_prec, "per_m": per_m,
             **({"per_call": per_call} if grouped else {"per_kernel": per_kernel}),
             "weight_pack": {"ms": round(wpack_ms, 3), "GB/s": round(wpack_bytes / (wpack_ms * 1e-3) / 1e9, 1)}}
@@ -478,7 +485,7 @@ def main():
     log("baselines")
     if not args.no_baselines:
         line.update(baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout,
-                              value, barrier, decode_gemms))
+                              value, barrier, decode_gemms, (per_call or {}).get("value")))
     clocks = sampler.summary(t_start, t_end)
     sampler.stop()
     line["clocks"] = clocks
@@ -763,7 +770,7 @@ def grouped_breakdown(torch, stream, decode_gemms, prec_idx, a_of, s_of, o_of, s
 
 
 def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_scale, cfgs, layout, value, barrier,
-              decode_gemms):
+              decode_gemms, per_call_value=None):
     """e2e through the public API with host buffers; cuBLAS FP16 / INT8 on the same cases; the CPU
     oracle on a bounded sample (rank 0, N=1)."""
     import torch
@@ -792,6 +799,19 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
     bufs = {key: P.alloc_packed(key[0], key[2], key[1], dev, digits=True) for key in keys}
     q_scale = {key: torch.empty(key[0], dtype=torch.float32, device=dev) for key in keys}
 
+    def e2e_packs(d_a, fp16):
+        """The step's 12 activation packs (quantize + pack from fp16, or pack from int8 codes): one
+        apt_pack_grouped launch on the grouped path, 12 single calls on the per-call path."""
+        if args.decode == "grouped":
+            P.pack_grouped([dict(x=d_a[key], bits=key[1], out=bufs[key], scale=q_scale[key]) if fp16 else
+                            dict(codes=d_a[key], bits=key[1], out=bufs[key]) for key in keys], stream=stream)
+            return
+        for key in keys:
+            if fp16:
+                P.quantize_pack(d_a[key], key[1], out=bufs[key], scale=q_scale[key])
+            else:
+                P.pack(d_a[key], key[1], out=bufs[key])
+
     def e2e_leg(fp16):
         if fp16:
             h_in = torch.empty(off, dtype=torch.float16).pin_memory()
@@ -807,11 +827,7 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
 
         def e2e_step(wset):
             d_in.copy_(h_in, non_blocking=True)
-            for key in keys:
-                if fp16:
-                    P.quantize_pack(d_a[key], key[1], out=bufs[key], scale=q_scale[key])
-                else:
-                    P.pack(d_a[key], key[1], out=bufs[key])
+            e2e_packs(d_a, fp16)
             decode_gemms(args.decode, wset, lambda i: bufs[(CASES[i][0], CASES[i][2], CASES[i][4])],
                          lambda i: q_scale[(CASES[i][0], CASES[i][2], CASES[i][4])] if fp16 else A_scale[CASES[i][0]],
                          lambda i: d_out[i], gather=False)
@@ -839,8 +855,10 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
         barrier()
         e2e_ms = s0.elapsed_time(s1) / n_e2e
         gm = "4x apt_gemm_grouped (36 GEMMs, fp16)" if args.decode == "grouped" else "36x apt_gemm (fp16)"
-        path = (f"pinned host fp16 activations -> 1 H2D -> 12x apt_quantize_pack -> {gm} -> 1 D2H"
-                if fp16 else f"pinned host int8 codes -> 1 H2D -> 12x apt_pack_bipolar -> {gm} -> 1 D2H")
+        qp = "apt_pack_grouped (12 quantize + packs)" if args.decode == "grouped" else "12x apt_quantize_pack"
+        pp = "apt_pack_grouped (12 packs)" if args.decode == "grouped" else "12x apt_pack_bipolar"
+        path = (f"pinned host fp16 activations -> 1 H2D -> {qp} -> {gm} -> 1 D2H"
+                if fp16 else f"pinned host int8 codes -> 1 H2D -> {pp} -> {gm} -> 1 D2H")
         return {"value": round(ops_step / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TOPS",
                 "h2d_bytes_per_step": h_in.numel() * h_in.element_size(), "d2h_bytes_per_step": o_total * 2,
                 "ms_per_step": round(e2e_ms, 5), "steps": n_e2e, "path": path + ", CUDA graph"}
@@ -874,11 +892,7 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
                 o2 += a_ * b_
 
             def comp(b=b, d_a=d_a, outs_b=outs_b):
-                for key in keys:
-                    if fp16:
-                        P.quantize_pack(d_a[key], key[1], out=bufs[key], scale=q_scale[key])
-                    else:
-                        P.pack(d_a[key], key[1], out=bufs[key])
+                e2e_packs(d_a, fp16)
                 decode_gemms(args.decode, b, lambda i: bufs[(CASES[i][0], CASES[i][2], CASES[i][4])],
                              lambda i: q_scale[(CASES[i][0], CASES[i][2], CASES[i][4])] if fp16 else A_scale[CASES[i][0]],
                              lambda i: outs_b[i], gather=False)
@@ -928,8 +942,10 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
         barrier()
         e2e_ms = s0.elapsed_time(s1) / n_e2e
         gm = "4x apt_gemm_grouped (36 GEMMs, fp16)" if args.decode == "grouped" else "36x apt_gemm (fp16)"
-        path = (f"pinned host fp16 activations -> H2D -> 12x apt_quantize_pack -> {gm} -> D2H" if fp16
-                else f"pinned host int8 codes -> H2D -> 12x apt_pack_bipolar -> {gm} -> D2H")
+        qp = "apt_pack_grouped (12 quantize + packs)" if args.decode == "grouped" else "12x apt_quantize_pack"
+        pp = "apt_pack_grouped (12 packs)" if args.decode == "grouped" else "12x apt_pack_bipolar"
+        path = (f"pinned host fp16 activations -> H2D -> {qp} -> {gm} -> D2H" if fp16
+                else f"pinned host int8 codes -> H2D -> {pp} -> {gm} -> D2H")
         return {"value": round(ops_step / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TOPS",
                 "h2d_bytes_per_step": off * (2 if fp16 else 1), "d2h_bytes_per_step": o_total * 2,
                 "ms_per_step": round(e2e_ms, 5), "steps": n_e2e,
@@ -966,6 +982,11 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
             del wi
             res["speedup_vs_cublas_fp16"] = round(value / res["cublas_fp16"]["value"], 3)
             res["speedup_vs_cublas_int8"] = round(value / res["cublas_int8"]["value"], 3)
+            res["cublas_note"] = ("cuBLAS runs the 36 GEMMs as 36 launches (torch exposes no grouped GEMM for mixed "
+                                  "shapes); the like-for-like per-launch ratio is per_call_speedup_*")
+            if per_call_value:
+                res["per_call_speedup_vs_cublas_fp16"] = round(per_call_value / res["cublas_fp16"]["value"], 3)
+                res["per_call_speedup_vs_cublas_int8"] = round(per_call_value / res["cublas_int8"]["value"], 3)
         except Exception as exc:
             res["cublas_error"] = repr(exc)
 

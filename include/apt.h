@@ -56,8 +56,9 @@
 extern "C" {
 #endif
 
-#define APT_ABI_VERSION 5
+#define APT_ABI_VERSION 6
 #define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
+#define APT_GROUP_MAX 64     /* problems per grouped call (apt_pack_grouped, apt_gemm_grouped) */
 
 typedef enum {
   APT_OK = 0,
@@ -150,6 +151,33 @@ APT_API apt_status apt_pack_bipolar(const int8_t* codes, int32_t rows, int32_t k
  *         a 1-bit symmetric grid has no positive level —, misaligned planes/digits), APT_ERR_CUDA. */
 APT_API apt_status apt_quantize_pack(const uint16_t* x, int32_t rows, int32_t k, int64_t ld, int32_t bits,
                                      apt_packed* out, float* scale, void* stream);
+
+/* Grouped activation packs: `count` independent apt_pack_bipolar (quantize == 0) / apt_quantize_pack
+ * (quantize == 1) calls in ONE launch (the activations of several decode GEMMs), each with exactly the
+ * semantics and outputs of its single call (§4.1 Steps 1-3; the quantization of P:199-201,
+ * reading R-Q).  Per problem:
+ *   src         : int8 codes (quantize == 0, signed encoding) or fp16 activations (quantize == 1), [rows][ld];
+ *   rows        : 1 .. APT_PACK_GROUP_MAX_ROWS (activation matrices: the one-word-per-thread pack);
+ *   bits        : 1..8 (2..8 with quantize);
+ *   out         : host struct as for apt_pack_bipolar, APT_PACK_ROWS layout, digit view REQUIRED (the
+ *                 packs are activation operands and release their dependents early, see "General contract");
+ *   scale       : quantize: device fp32 [rows] written (pass it as the GEMM's a_scale); else NULL;
+ *   range_error : codes only, nullable device int32 (as apt_pack_bipolar).
+ * Errors: APT_ERR_INVALID_ARGUMENT (count outside [1, APT_GROUP_MAX], a problem violating the above),
+ *         APT_ERR_CUDA. */
+#define APT_PACK_GROUP_MAX_ROWS 64
+typedef struct {
+  const void* src;
+  int32_t quantize;
+  int32_t rows;
+  int32_t k;
+  int32_t bits;
+  int64_t ld;
+  apt_packed* out;
+  float* scale;
+  int32_t* range_error;
+} apt_pack_problem;
+APT_API apt_status apt_pack_grouped(int32_t count, const apt_pack_problem* problems /* host */, void* stream);
 
 /* Per-channel / per-token fp32 scales for APT_OUT_F16_SCALED (reading Q10):
  *   out[m][n] = RN_fp16( ((float)Y[m][n] * w_scale[n]) * a_scale[m] ), fp32 arithmetic,
@@ -323,7 +351,6 @@ APT_API apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int3
  *               workspace serves both kinds of call on one stream).
  * Errors: APT_ERR_INVALID_ARGUMENT (count outside [1, APT_GROUP_MAX], a problem violating the above),
  *         APT_ERR_UNSUPPORTED (int32 bound), APT_ERR_WORKSPACE, APT_ERR_CUDA. */
-#define APT_GROUP_MAX 64
 typedef struct {
   int32_t M, N, K, wbits, abits;
   apt_packed W;

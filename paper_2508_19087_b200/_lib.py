@@ -16,13 +16,13 @@ APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
 APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
 APT_KERNEL_AUTO, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY, APT_KERNEL_DEC, APT_KERNEL_PF = 0, 2, 3, 4, 5, 6
 APT_MMA_I8, APT_MMA_MXF4 = 0, 1
-ABI_VERSION = 5  # include/apt.h APT_ABI_VERSION this binding marshals for
+ABI_VERSION = 6  # include/apt.h APT_ABI_VERSION this binding marshals for
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes", "apt_gemm_zp_workspace_bytes",
             "apt_gemm", "apt_status_string", "apt_abi_version", "apt_table_load", "apt_table_clear", "apt_table_size",
             "apt_table_lookup", "apt_enumerate_configs", "apt_recombine_plane_products",
-            "apt_gemm_grouped_workspace_bytes", "apt_gemm_grouped"]
+            "apt_gemm_grouped_workspace_bytes", "apt_gemm_grouped", "apt_pack_grouped"]
 
 
 class AptPacked(ctypes.Structure):
@@ -43,6 +43,13 @@ class AptGemmProblem(ctypes.Structure):
 
 
 APT_GROUP_MAX = 64
+APT_PACK_GROUP_MAX_ROWS = 64
+
+
+class AptPackProblem(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("quantize", ctypes.c_int32), ("rows", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("bits", ctypes.c_int32), ("ld", ctypes.c_int64), ("out", ctypes.POINTER(AptPacked)),
+                ("scale", ctypes.c_void_p), ("range_error", ctypes.c_void_p)]
 
 
 class AptConfig(ctypes.Structure):
@@ -113,6 +120,8 @@ def lib():
         L.apt_gemm_grouped.restype = ctypes.c_int
         L.apt_gemm_grouped.argtypes = [ctypes.c_int32, ctypes.POINTER(AptGemmProblem), ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p]
+        L.apt_pack_grouped.restype = ctypes.c_int
+        L.apt_pack_grouped.argtypes = [ctypes.c_int32, ctypes.POINTER(AptPackProblem), ctypes.c_void_p]
         v = int(L.apt_abi_version())
         if v != ABI_VERSION:
             raise ImportError(f"{LIB_PATH} has ABI version {v}, this binding needs {ABI_VERSION}: rebuild it")

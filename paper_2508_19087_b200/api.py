@@ -342,3 +342,42 @@ def gemm_grouped(problems, workspace: torch.Tensor | None = None, stream=None) -
                                   _stream_handle(stream))
     L.check("apt_gemm_grouped", rc)
     return outs
+
+
+def pack_grouped(problems, stream=None) -> list:
+    """apt_pack_grouped: several independent ACTIVATION packs (digit views, <= 64 rows each) in one launch.
+
+    Each problem is a dict with ``out`` (a Packed with a digit view, e.g. ``alloc_packed(..., digits=True)``)
+    and ``bits``, plus either ``codes`` (int8 [rows, k], apt_pack_bipolar semantics) or ``x`` (fp16
+    [rows, k], apt_quantize_pack semantics, per-row scales written to ``scale``).  Returns the outs."""
+    problems = list(problems)
+    n = len(problems)
+    if not 1 <= n <= L.APT_GROUP_MAX:
+        raise ValueError(f"apt_pack_grouped takes 1..{L.APT_GROUP_MAX} problems, got {n}")
+    arr = (L.AptPackProblem * n)()
+    structs = []
+    for i, pr in enumerate(problems):
+        out, bits = pr["out"], int(pr["bits"])
+        quant = "x" in pr
+        src = pr["x"] if quant else pr["codes"]
+        _require_cuda(src, "x" if quant else "codes")
+        want = torch.float16 if quant else torch.int8
+        if src.dtype != want or src.dim() != 2 or src.stride(1) != 1:
+            raise ValueError(f"problem {i}: {'x' if quant else 'codes'} must be a 2-D {want} tensor with unit stride along K")
+        rows, k = src.shape
+        if out.digits is None or out.tiled:
+            raise ValueError(f"problem {i}: out must be a row-layout Packed with a digit view")
+        _check_out(out, rows, k, bits, False, True)
+        scale = pr.get("scale")
+        if quant and (scale is None or scale.dtype != torch.float32 or not scale.is_contiguous() or scale.numel() < rows):
+            raise ValueError(f"problem {i}: quantize needs a contiguous fp32 scale of >= rows elements")
+        st = out.struct()
+        structs.append(st)
+        p = arr[i]
+        p.src, p.quantize, p.rows, p.k, p.bits, p.ld = src.data_ptr(), int(quant), rows, k, bits, src.stride(0)
+        p.out = ctypes.pointer(st)
+        p.scale = scale.data_ptr() if quant else None
+        re_ = pr.get("range_error")
+        p.range_error = re_.data_ptr() if re_ is not None else None
+    L.check("apt_pack_grouped", L.lib().apt_pack_grouped(n, arr, _stream_handle(stream)))
+    return [pr["out"] for pr in problems]

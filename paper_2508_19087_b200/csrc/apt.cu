@@ -285,6 +285,49 @@ apt_status apt_quantize_pack(const uint16_t* x, int32_t rows, int32_t k, int64_t
   return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
 }
 
+apt_status apt_pack_grouped(int32_t count, const apt_pack_problem* problems, void* stream) {
+  if (count < 1 || count > APT_GROUP_MAX || count > apt::kPackGroupMax || !problems) return APT_ERR_INVALID_ARGUMENT;
+  static apt::PackGroupArgs ga_zero;  // zero-initialised template (the struct is ~10 KB)
+  apt::PackGroupArgs ga = ga_zero;
+  ga.count = count;
+  int ctas = 0, threads = 32;
+  for (int i = 0; i < count; ++i) {
+    const apt_pack_problem& P = problems[i];
+    apt_packed* out = P.out;
+    const bool quant = P.quantize != 0;
+    if (!P.src || !out || !out->planes || !out->row_sum || !out->digits) return APT_ERR_INVALID_ARGUMENT;
+    if (P.rows <= 0 || P.rows > APT_PACK_GROUP_MAX_ROWS || P.k <= 0 || P.ld < P.k) return APT_ERR_INVALID_ARGUMENT;
+    if (P.bits < (quant ? 2 : 1) || P.bits > 8 || (quant && !P.scale)) return APT_ERR_INVALID_ARGUMENT;
+    if (!aligned16(out->planes) || !aligned16(out->digits) || out->layout != APT_PACK_ROWS) return APT_ERR_INVALID_ARGUMENT;
+    out->rows = P.rows;
+    out->k = P.k;
+    out->k_words = (int32_t)(kpad_of(P.k) / 32);
+    out->bits = P.bits;
+    apt::PackArgs& p = ga.p[i];
+    p.codes = quant ? nullptr : reinterpret_cast<const int8_t*>(P.src);
+    p.ld = P.ld;
+    p.rows = P.rows;
+    p.k = P.k;
+    p.k_words = out->k_words;
+    p.enc = APT_ENC_SIGNED;
+    p.planes = out->planes;
+    p.tiled = 0;
+    p.plane_stride = (int64_t)P.rows * out->k_words;
+    p.row_sum = out->row_sum;
+    p.range_error = quant ? nullptr : P.range_error;
+    p.digits = out->digits;
+    ga.x[i] = quant ? P.src : nullptr;
+    ga.scale[i] = quant ? P.scale : nullptr;
+    ga.bits[i] = P.bits;
+    ga.rows_per_cta[i] = apt::pack_group_rows_per_cta(p);
+    ctas += (P.rows + ga.rows_per_cta[i] - 1) / ga.rows_per_cta[i];
+    ga.cta_end[i] = ctas;
+    threads = std::max(threads, apt::pack_group_threads(p));
+  }
+  cudaError_t err = apt::launch_pack_grouped(ga, ctas, threads, reinterpret_cast<cudaStream_t>(stream));
+  return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+}
+
 apt_status apt_select_config(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, apt_config* out) {
   if (!out || M <= 0 || N <= 0 || K <= 0 || wbits < 1 || wbits > 8 || abits < 1 || abits > 8)
     return APT_ERR_INVALID_ARGUMENT;

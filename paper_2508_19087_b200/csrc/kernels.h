@@ -24,6 +24,21 @@ cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream);
 // fused fp16 -> per-row symmetric quantize -> pack (x: const __half*, scale: [rows] fp32 out)
 cudaError_t launch_quant_pack(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream);
 
+// grouped activation packs (one word per thread, digit views): problem i owns CTAs [cta_end[i-1], cta_end[i])
+constexpr int kPackGroupMax = 64;
+struct PackGroupArgs {
+  int32_t count;
+  int32_t cta_end[kPackGroupMax];
+  int32_t rows_per_cta[kPackGroupMax];
+  int32_t bits[kPackGroupMax];
+  const void* x[kPackGroupMax];   // fp16 rows to quantize (apt_quantize_pack semantics), or null: int8 codes
+  float* scale[kPackGroupMax];    // per-row scales out (quantize)
+  PackArgs p[kPackGroupMax];
+};
+int pack_group_rows_per_cta(const PackArgs& p);
+int pack_group_threads(const PackArgs& p);
+cudaError_t launch_pack_grouped(const PackGroupArgs& a, int ctas, int threads, cudaStream_t stream);
+
 // activation planes [abits][M][k_words] -> kernel-order u8 digits [M][Kpad]
 cudaError_t launch_expand_tokens(const uint32_t* ap, int64_t a_pstride, int M, int k_words, int abits,
                                  uint8_t* out, cudaStream_t stream);

@@ -139,15 +139,12 @@ __device__ __forceinline__ void load_words(const PackArgs& p, const void* rowp, 
 
 // WPI = words per work item: 4 (a 128-element quad, one 16-byte store per plane: the weight packs,
 // bandwidth) or 1 (one 32-element word: the activation packs, a short per-thread critical path)
+// The rows [cta * R, cta * R + R) of one pack (the body of pack_kernel and of pack_grouped_kernel).
 template <int BITS, bool QUANT, int WPI>
-__global__ void __launch_bounds__(WPI == 1 ? kPackWordThreads : kPackThreads, WPI == 1 ? 1 : 2) pack_kernel(PackArgs p, const __half* __restrict__ x, float* scale,
-                                                             int rows_per_cta) {
-  if (p.digits) pdl_launch_dependents();  // activation operand: see pack_release()
-  pdl_wait();  // our codes / output buffers may still be in use by the previous kernel
-  __shared__ int s_sum[kPackMaxRows];
-  __shared__ unsigned s_amax[kPackMaxRows];
+__device__ __forceinline__ void pack_body(const PackArgs& p, const __half* __restrict__ x, float* scale,
+                                          int rows_per_cta, int cta, int* s_sum, unsigned* s_amax) {
   const int R = rows_per_cta;
-  const int r0 = blockIdx.x * R;
+  const int r0 = cta * R;
   const int Q = p.k_words / WPI;  // work items per row
   const int items = R * Q;
   constexpr int kQmax = (1 << (BITS - 1)) - 1;
@@ -281,7 +278,42 @@ __global__ void __launch_bounds__(WPI == 1 ? kPackWordThreads : kPackThreads, WP
   __syncthreads();
   for (int i = threadIdx.x; i < R; i += blockDim.x)
     if (r0 + i < p.rows) p.row_sum[r0 + i] = s_sum[i];
+}
+
+template <int BITS, bool QUANT, int WPI>
+__global__ void __launch_bounds__(WPI == 1 ? kPackWordThreads : kPackThreads, WPI == 1 ? 1 : 2) pack_kernel(PackArgs p, const __half* __restrict__ x, float* scale,
+                                                             int rows_per_cta) {
+  if (p.digits) pdl_launch_dependents();  // activation operand: see pack_release()
+  pdl_wait();  // our codes / output buffers may still be in use by the previous kernel
+  __shared__ int s_sum[kPackMaxRows];
+  __shared__ unsigned s_amax[kPackMaxRows];
+  pack_body<BITS, QUANT, WPI>(p, x, scale, rows_per_cta, blockIdx.x, s_sum, s_amax);
   if (!p.digits) pack_release();
+}
+
+// Grouped activation packs (apt_pack_grouped): several independent packs WITH digit views in one launch;
+// CTA b belongs to the problem i with cta_end[i - 1] <= b < cta_end[i] and packs that problem's rows
+// exactly as its own pack_kernel launch would (one word per thread).  Activation operands only, so the
+// launch releases its dependents at entry like every digit-view pack.
+__global__ void __launch_bounds__(kPackWordThreads, 1) pack_grouped_kernel(const __grid_constant__ PackGroupArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
+  __shared__ int s_sum[kPackMaxRows];
+  __shared__ unsigned s_amax[kPackMaxRows];
+  int i = 0;
+  while (i + 1 < a.count && (int)blockIdx.x >= a.cta_end[i]) ++i;
+  const int cta = (int)blockIdx.x - (i ? a.cta_end[i - 1] : 0);
+  const PackArgs& p = a.p[i];
+  const __half* x = reinterpret_cast<const __half*>(a.x[i]);
+  const int R = a.rows_per_cta[i];
+  switch (a.bits[i] * 2 + (a.x[i] ? 1 : 0)) {
+#define APT_PG(B)                                                                          \
+  case 2 * B: pack_body<B, false, 1>(p, x, a.scale[i], R, cta, s_sum, s_amax); break;      \
+  case 2 * B + 1: if (B > 1) pack_body<B, true, 1>(p, x, a.scale[i], R, cta, s_sum, s_amax); break;
+    APT_PG(1) APT_PG(2) APT_PG(3) APT_PG(4) APT_PG(5) APT_PG(6) APT_PG(7) APT_PG(8)
+#undef APT_PG
+    default: break;
+  }
 }
 
 // rows per CTA: whole rows (row sums without global atomics); tile-major weights: 32 rows so a warp's
@@ -326,6 +358,13 @@ template <bool QUANT>
 static cudaError_t launch_pack_t(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {
   if (p.digits && p.rows <= APT_PACK_WORD_ROWS) return launch_pack_w<QUANT, 1>(p, x, scale, bits, stream);
   return launch_pack_w<QUANT, 4>(p, x, scale, bits, stream);
+}
+
+int pack_group_rows_per_cta(const PackArgs& p) { return pack_rows_per_cta(p, 1); }
+int pack_group_threads(const PackArgs& p) { return pack_threads(p, 1); }
+
+cudaError_t launch_pack_grouped(const PackGroupArgs& a, int ctas, int threads, cudaStream_t stream) {
+  return launch_pdl(pack_grouped_kernel, dim3(ctas), dim3(threads), 0, stream, dim3(1, 1, 1), a);
 }
 
 cudaError_t launch_pack(const PackArgs& p, int bits, cudaStream_t stream) {

@@ -171,3 +171,77 @@ def test_grouped_rejects():
             P.gemm_grouped([pr, bad])
     with pytest.raises(ValueError):
         P.gemm_grouped([pr] * 65)
+
+
+# ----------------------------------------------------------------------------- grouped activation packs
+
+PACK_CASES = [(1, 4096, 2), (8, 4096, 4), (16, 11008, 2), (3, 33, 1), (5, 257, 8), (64, 4096, 3), (16, 11008, 4),
+              (2, 700, 5), (1, 1, 6), (9, 1300, 7)]
+
+
+def test_pack_grouped_codes_matches_oracle_and_single():
+    """apt_pack_grouped (int8 codes) == oracle.pack_planes (planes, row sums) and == the single-call
+    apt_pack_bipolar digit view, bit for bit, for every problem of a mixed-width, ragged group."""
+    prs, ref = [], []
+    for i, (rows, k, bits) in enumerate(PACK_CASES):
+        c = signed_codes(rows, k, bits, seed=300 + i)
+        prs.append(dict(codes=_dev(c), bits=bits, out=P.alloc_packed(rows, k, bits, DEV, digits=True)))
+        ref.append(c)
+    P.pack_grouped(prs)
+    torch.cuda.synchronize()
+    for pr, c, (rows, k, bits) in zip(prs, ref, PACK_CASES):
+        planes, rs = O.pack_planes(c, bits)
+        out = pr["out"]
+        assert np.array_equal(out.planes.cpu().numpy().view(np.uint32), planes)
+        assert np.array_equal(out.row_sum.cpu().numpy().astype(np.int64), rs)
+        one = P.pack(pr["codes"], bits, digits=True)
+        assert torch.equal(one.digits, out.digits)
+
+
+def test_pack_grouped_quantize_matches_oracle():
+    """apt_pack_grouped (fp16, quantize) == oracle.quantize_symmetric + pack_planes: scales, planes, row
+    sums bit-exact, digit view == the single-call apt_quantize_pack's."""
+    from synth import fp16_activations
+    prs, xs = [], []
+    for i, (rows, k, bits) in enumerate(PACK_CASES):
+        bits = max(bits, 2)
+        x = fp16_activations(rows, k, seed=700 + i)
+        prs.append(dict(x=_dev(x), bits=bits, out=P.alloc_packed(rows, k, bits, DEV, digits=True),
+                        scale=torch.empty(rows, dtype=torch.float32, device=DEV)))
+        xs.append(x)
+    P.pack_grouped(prs)
+    torch.cuda.synchronize()
+    for pr, x in zip(prs, xs):
+        bits = pr["bits"]
+        codes, so = O.quantize_symmetric(x, bits)
+        planes, rs = O.pack_planes(codes, bits)
+        assert np.array_equal(pr["scale"].cpu().numpy(), so)
+        assert np.array_equal(pr["out"].planes.cpu().numpy().view(np.uint32), planes)
+        assert np.array_equal(pr["out"].row_sum.cpu().numpy().astype(np.int64), rs)
+        one, _ = P.quantize_pack(pr["x"], bits)
+        assert torch.equal(one.digits, pr["out"].digits)
+
+
+def test_pack_grouped_then_gemm_grouped_stream_order():
+    """The bench's step on one stream, 30 times with fresh codes each time: grouped packs straight into the
+    grouped GEMM's activation buffers, every output equal to the C oracle."""
+    cases = [(16, 4096, 4096, 2, 2), (8, 11008, 4096, 4, 4), (1, 4096, 11008, 1, 2)]
+    W = [signed_codes(n, k, pw, seed=900 + i) for i, (m, n, k, pw, pa) in enumerate(cases)]
+    prs = [dict(W=P.pack(_dev(w), pw, tiled=True), A=P.alloc_packed(m, k, pa, DEV, digits=True))
+           for w, (m, n, k, pw, pa) in zip(W, cases)]
+    for it in range(30):
+        a = [signed_codes(m, k, pa, seed=5000 + 3 * it + i) for i, (m, n, k, pw, pa) in enumerate(cases)]
+        P.pack_grouped([dict(codes=_dev(ai), bits=c[4], out=pr["A"]) for ai, c, pr in zip(a, cases, prs)])
+        outs = P.gemm_grouped(prs)
+        if it % 10 == 9:
+            for out, ai, w in zip(outs, a, W):
+                assert np.array_equal(out.cpu().numpy().astype(np.int64), c_gemm_i64(ai, w))
+
+
+def test_pack_grouped_rejects():
+    c = _dev(signed_codes(4, 256, 2, seed=1))
+    with pytest.raises(ValueError):  # no digit view
+        P.pack_grouped([dict(codes=c, bits=2, out=P.alloc_packed(4, 256, 2, DEV))])
+    big = _dev(signed_codes(65, 256, 2, seed=2))  # more rows than the one-word-per-thread pack takes
+    with pytest.raises(P._lib.AptError):
+        P.pack_grouped([dict(codes=big, bits=2, out=P.alloc_packed(65, 256, 2, DEV, digits=True))])
