@@ -297,6 +297,28 @@ def quantize_symmetric(x: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray]:
     return codes, scales
 
 
+def group_dequant_gemm_fp64(a_codes: np.ndarray, w_codes: np.ndarray, w_gscale, a_gscale=None, a_scale=None,
+                            group: int = 128) -> np.ndarray:
+    """Group-wise scales (the 128-group configurations Atom-128G / QuaRot-128G of the
+    PPL table, with the linear quantization x = s x_hat of P:199-201 applied per K-group):
+    element k of a row belongs to group g = k // group; the weights dequantize as
+    W[n][k] = w_gscale[g][n] * w_hat[n][k] and the activations as A[m][k] = a_gscale[g][m] * a_hat[m][k]
+    (or a_scale[m] * a_hat[m][k] on every group when a_gscale is None; scale 1 when both are None).  The
+    plain definition, in fp64: dequantize both operands, then out = A . W^T.  w_gscale: [ceil(K/group)][N]
+    fp32 (group-major, the GPTQ layout), a_gscale: [ceil(K/group)][M]."""
+    m, k = a_codes.shape
+    n = w_codes.shape[0]
+    gi = np.arange(k) // group                                   # group of every K element
+    wg = np.asarray(w_gscale, dtype=np.float64)                  # [G][N]
+    Wd = wg[gi, :].T * w_codes.astype(np.float64)                # [N][K]
+    if a_gscale is not None:
+        Ad = np.asarray(a_gscale, dtype=np.float64)[gi, :].T * a_codes.astype(np.float64)
+    else:
+        sa = np.ones(m) if a_scale is None else np.asarray(a_scale, dtype=np.float64)
+        Ad = sa[:, None] * a_codes.astype(np.float64)
+    return Ad @ Wd.T
+
+
 def dequant_gemm_fp64(a_codes: np.ndarray, w_codes: np.ndarray, w_scale, a_scale, w_zero=None,
                       a_zero=None) -> np.ndarray:
     """P:199-201 linear quantization with zero points on both operands, the plain

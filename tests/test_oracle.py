@@ -396,3 +396,45 @@ def test_dequant_gemm_exact_brute_force():
                 assert abs(Fraction(got[i, j]) - ex) <= Fraction(1, 1 << 40) * (1 + abs(ex))
         assert np.allclose(O.dequant_gemm_fp64(a, w, ws, as_), O.scale_fp64(O.gemm_signed(a, w), ws, as_),
                            rtol=1e-14, atol=0)
+
+
+def test_group_dequant_gemm_exact_brute_force():
+    """group_dequant_gemm_fp64 vs exact rational brute force sum_k (s_a[g(k)] x)(s_w[g(k)] w) with
+    g(k) = k // group on tiny inputs spanning several groups (group sizes 4 and 128), with and without
+    activation group scales."""
+    rng = np.random.default_rng(12)
+    for it in range(16):
+        group = 4 if it % 2 else 128
+        m, n = (int(v) for v in rng.integers(1, 4, size=2))
+        k = int(rng.integers(1, 3 * group + 2))
+        G = -(-k // group)
+        a = signed_codes(m, k, 4, seed=int(rng.integers(1 << 30)))
+        w = signed_codes(n, k, 3, seed=int(rng.integers(1 << 30)))
+        wg = rng.uniform(0.01, 1, (G, n)).astype(np.float32)
+        ag = rng.uniform(0.01, 1, (G, m)).astype(np.float32) if it % 4 < 2 else None
+        sa = rng.uniform(0.01, 1, m).astype(np.float32)
+        got = O.group_dequant_gemm_fp64(a, w, wg, ag, None if ag is not None else sa, group=group)
+        for i in range(m):
+            for j in range(n):
+                ex = Fraction(0)
+                for q in range(k):
+                    g = q // group
+                    s_a = Fraction(float(ag[g, i])) if ag is not None else Fraction(float(sa[i]))
+                    ex += s_a * int(a[i, q]) * Fraction(float(wg[g, j])) * int(w[j, q])
+                assert abs(Fraction(got[i, j]) - ex) <= Fraction(1, 1 << 40) * (1 + abs(ex))
+
+
+def test_group_dequant_gemm_reduces_to_per_channel():
+    """Equal scales on every group reduce to the per-channel / per-token epilogue (scale_fp64 of the
+    exact int64 product), and a single group (K <= 128) to dequant_gemm_fp64 with that group's scales."""
+    rng = np.random.default_rng(13)
+    a = signed_codes(5, 700, 4, seed=1)
+    w = signed_codes(9, 700, 2, seed=2)
+    ws, as_ = rng.uniform(0.01, 1, 9).astype(np.float32), rng.uniform(0.01, 1, 5).astype(np.float32)
+    G = -(-700 // 128)
+    got = O.group_dequant_gemm_fp64(a, w, np.tile(ws, (G, 1)), np.tile(as_, (G, 1)))
+    assert np.allclose(got, O.scale_fp64(O.gemm_signed(a, w), ws, as_), rtol=1e-13, atol=0)
+    a1, w1 = a[:, :100], w[:, :100]
+    wg, ag = rng.uniform(0.01, 1, (1, 9)).astype(np.float32), rng.uniform(0.01, 1, (1, 5)).astype(np.float32)
+    assert np.allclose(O.group_dequant_gemm_fp64(a1, w1, wg, ag), O.dequant_gemm_fp64(a1, w1, wg[0], ag[0]),
+                       rtol=1e-13, atol=0)
