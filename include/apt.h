@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define APT_ABI_VERSION 6
+#define APT_ABI_VERSION 7
 #define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
 #define APT_GROUP_MAX 64     /* problems per grouped call (apt_pack_grouped, apt_gemm_grouped) */
 
@@ -190,11 +190,26 @@ APT_API apt_status apt_pack_grouped(int32_t count, const apt_pack_problem* probl
  * int32 Y into the workspace and a second elementwise pass applies the formula, so the workspace
  * must hold apt_gemm_zp_workspace_bytes(); without them nothing changes.  Zero points are ignored
  * for the int32 output kinds. */
+/* Group-wise scales (the 128-group configurations of the paper's PPL table, P:655-656,
+ * i.e. the linear quantization of P:199-201 applied per K-group g = k / 128), APT_OUT_F16_SCALED only:
+ *   out[m][n] = RN_fp16( sum_g ((float)Y_g[m][n] * w_gscale[g][n]) * a_g[m] ),  Y_g = sum_{k in g} A W exact,
+ *   a_g[m] = a_gscale[g][m] (or a_scale[m] / 1 when a_gscale is NULL), fp32 sums over g in order.
+ * group_size = 128 selects it (0 = per-channel scales as above; w_scale is then ignored); zero points are
+ * not combined with group scales.  w_gscale: fp32 [Kpad/128][N] (group-major, the GPTQ layout), a_gscale:
+ * fp32 [Kpad/128][M] or NULL.  The GEMM computes every group's exact product on signed digits in the
+ * grouped decode kernel (gemm_grp.cu; any M, in chunks of 16 tokens): W in the APT_PACK_TILED layout and A
+ * with its digit view are required (else APT_ERR_UNSUPPORTED), and the workspace must hold
+ * apt_gemm_grouped_workspace_bytes(1) (else APT_ERR_WORKSPACE).
+ * Zero points at M <= 16 with a tiled W, a digit-view A, no forced config and such a workspace are fused
+ * into the same kernel's epilogue (one launch, the formula above evaluated identically). */
 typedef struct {
-  const float* w_scale; /* [N], required for APT_OUT_F16_SCALED */
-  const float* a_scale; /* [M] per token, or NULL (== 1)        */
-  const float* w_zero;  /* [N] per output channel, or NULL (== 0) */
-  const float* a_zero;  /* [M] per token, or NULL (== 0)          */
+  const float* w_scale;  /* [N], required for APT_OUT_F16_SCALED unless group_size != 0 */
+  const float* a_scale;  /* [M] per token, or NULL (== 1)        */
+  const float* w_zero;   /* [N] per output channel, or NULL (== 0) */
+  const float* a_zero;   /* [M] per token, or NULL (== 0)          */
+  const float* w_gscale; /* [Kpad/128][N] group scales (group_size == 128), else NULL */
+  const float* a_gscale; /* [Kpad/128][M] or NULL                  */
+  int32_t group_size;    /* 0 (per channel) or 128                 */
 } apt_scales;
 
 typedef enum {
@@ -343,7 +358,8 @@ APT_API apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int3
  * Per problem (apt_gemm_problem, host array):
  *   M in [1, 16]; W = apt_pack_bipolar output in APT_PACK_TILED layout without a digit view; A = an
  *   APT_PACK_ROWS activation WITH its digit view; kind / layout / out / ldo / scales as apt_gemm
- *   (zero points are not supported here: w_zero and a_zero must be NULL); 1 <= wbits, abits <= 8 and
+ *   (zero points fused into the epilogue; group-wise scales: every problem of the call with
+ *   group_size 128, or none); 1 <= wbits, abits <= 8 and
  *   Kpad * 255 * 255 < 2^32 (the digits are u * 2^s).
  * The problems must not overlap: no problem's `out` may alias another problem's inputs or output.
  *   workspace : device, >= apt_gemm_grouped_workspace_bytes(count), 16-byte aligned; its first

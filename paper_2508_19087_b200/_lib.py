@@ -16,7 +16,7 @@ APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
 APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
 APT_KERNEL_AUTO, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY, APT_KERNEL_DEC, APT_KERNEL_PF = 0, 2, 3, 4, 5, 6
 APT_MMA_I8, APT_MMA_MXF4 = 0, 1
-ABI_VERSION = 6  # include/apt.h APT_ABI_VERSION this binding marshals for
+ABI_VERSION = 7  # include/apt.h APT_ABI_VERSION this binding marshals for
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes", "apt_gemm_zp_workspace_bytes",
@@ -33,7 +33,8 @@ class AptPacked(ctypes.Structure):
 
 class AptScales(ctypes.Structure):
     _fields_ = [("w_scale", ctypes.c_void_p), ("a_scale", ctypes.c_void_p), ("w_zero", ctypes.c_void_p),
-                ("a_zero", ctypes.c_void_p)]
+                ("a_zero", ctypes.c_void_p), ("w_gscale", ctypes.c_void_p), ("a_gscale", ctypes.c_void_p),
+                ("group_size", ctypes.c_int32)]
 
 
 class AptGemmProblem(ctypes.Structure):

@@ -237,9 +237,11 @@ def workspace_bytes(cfg: dict, M: int, N: int, K: int) -> int:
 def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_scale: torch.Tensor | None = None,
          a_scale: torch.Tensor | None = None, out: torch.Tensor | None = None, config: dict | None = None,
          workspace: torch.Tensor | None = None, stream=None, w_zero: torch.Tensor | None = None,
-         a_zero: torch.Tensor | None = None) -> torch.Tensor:
+         a_zero: torch.Tensor | None = None, w_gscale: torch.Tensor | None = None,
+         a_gscale: torch.Tensor | None = None) -> torch.Tensor:
     """apt_gemm: Y = A . W^T (exact int32), Y' (bipolar), or fp16-scaled, in row ([M,N]) or col
-    ([N,M]) layout."""
+    ([N,M]) layout.  ``w_gscale`` ([Kpad/128, N] fp32) / ``a_gscale`` ([Kpad/128, M]) select group-wise
+    (128) scales for the fp16 output (include/apt.h apt_scales)."""
     M, N, K = A.rows, W.rows, W.k
     if A.k != K:
         raise ValueError("A and W have different K")
@@ -253,16 +255,10 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
         out = torch.empty(shape, dtype=dtype, device=W.planes.device)
     if out.dtype != dtype or out.dim() != 2 or out.stride(1) != 1 or tuple(out.shape) != shape:
         raise ValueError(f"out must be a {dtype} tensor of shape {shape} with unit inner stride")
-    sc = None
-    if any(t is not None for t in (w_scale, a_scale, w_zero, a_zero)):
-        for t, nm in ((w_scale, "w_scale"), (a_scale, "a_scale"), (w_zero, "w_zero"), (a_zero, "a_zero")):
-            if t is not None:
-                _require_cuda(t, nm)
-                if t.dtype != torch.float32 or not t.is_contiguous():
-                    raise ValueError(f"{nm} must be contiguous fp32")
-        sc = L.AptScales(*(t.data_ptr() if t is not None else None for t in (w_scale, a_scale, w_zero, a_zero)))
+    sc = _scales_struct(w_scale, a_scale, w_zero, a_zero, w_gscale, a_gscale, K, N, M)
     c = _config_struct(config)
     zp = kind == L.APT_OUT_F16_SCALED and (w_zero is not None or a_zero is not None)
+    gs = w_gscale is not None
     cc = c
     if cc is None:
         cc = L.AptConfig()
@@ -271,6 +267,9 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
     ws_need = int(fn(ctypes.byref(cc), M, N, K))
     if A.digits is not None and not zp and cc.kernel != L.APT_KERNEL_DEC and cc.mma_kind != L.APT_MMA_MXF4:
         ws_need = 0  # the digit view replaces the token expansion area (kind::mxf4 expands e2m1 tokens)
+    if gs or (zp and M <= 16 and W.tiled and A.digits is not None and config is None):
+        # the grouped kernel's route (group scales; zero points fused at decode token counts)
+        ws_need = max(ws_need, int(L.lib().apt_gemm_grouped_workspace_bytes(1)))
     if ws_need > 0 and (workspace is None or workspace.numel() * workspace.element_size() < ws_need):
         if workspace is not None:
             raise ValueError(f"workspace holds {workspace.numel() * workspace.element_size()} bytes, "
@@ -286,6 +285,23 @@ def gemm(W: Packed, A: Packed, out_kind: str = "i32", layout: str = "row", w_sca
     return out
 
 
+def _scales_struct(w_scale, a_scale, w_zero, a_zero, w_gscale, a_gscale, K, N, M):
+    """apt_scales from fp32 device tensors (None = NULL); group scales [Kpad/128, N] / [Kpad/128, M]."""
+    ts = (("w_scale", w_scale, N), ("a_scale", a_scale, M), ("w_zero", w_zero, N), ("a_zero", a_zero, M),
+          ("w_gscale", w_gscale, kpad(K) // 128 * N), ("a_gscale", a_gscale, kpad(K) // 128 * M))
+    if all(t is None for _, t, _ in ts):
+        return None
+    for nm, t, size in ts:
+        if t is not None:
+            _require_cuda(t, nm)
+            if t.dtype != torch.float32 or not t.is_contiguous() or t.numel() < size:
+                raise ValueError(f"{nm} must be a contiguous fp32 tensor of >= {size} elements")
+    if a_gscale is not None and w_gscale is None:
+        raise ValueError("a_gscale needs w_gscale (group-wise scales)")
+    return L.AptScales(*(t.data_ptr() if t is not None else None for _, t, _ in ts),
+                       128 if w_gscale is not None else 0)
+
+
 def grouped_workspace(device) -> torch.Tensor:
     """A zero-initialised workspace large enough for apt_gemm_grouped (and, since its ticket area is
     shared, usable by apt_gemm calls on the same stream as well)."""
@@ -298,7 +314,8 @@ def gemm_grouped(problems, workspace: torch.Tensor | None = None, stream=None) -
 
     ``problems`` is a sequence of dicts with the keys of :func:`gemm`: ``W`` (tile-major Packed),
     ``A`` (Packed with its digit view), and optionally ``out_kind``, ``layout``, ``w_scale``,
-    ``a_scale``, ``out``.  Returns the list of outputs; each equals ``gemm`` on the same arguments."""
+    ``a_scale``, ``w_zero``, ``a_zero``, ``w_gscale``, ``a_gscale``, ``out``.  Returns the list of
+    outputs; each equals ``gemm`` on the same arguments."""
     problems = list(problems)
     n = len(problems)
     if not 1 <= n <= L.APT_GROUP_MAX:
@@ -323,17 +340,13 @@ def gemm_grouped(problems, workspace: torch.Tensor | None = None, stream=None) -
             out = torch.empty(shape, dtype=dtype, device=dev)
         if out.dtype != dtype or out.dim() != 2 or out.stride(1) != 1 or tuple(out.shape) != shape:
             raise ValueError(f"problem {i}: out must be a {dtype} tensor of shape {shape} with unit inner stride")
-        ws_, as_ = pr.get("w_scale"), pr.get("a_scale")
-        for t, nm in ((ws_, "w_scale"), (as_, "a_scale")):
-            if t is not None:
-                _require_cuda(t, nm)
-                if t.dtype != torch.float32 or not t.is_contiguous():
-                    raise ValueError(f"problem {i}: {nm} must be contiguous fp32")
+        sc = _scales_struct(pr.get("w_scale"), pr.get("a_scale"), pr.get("w_zero"), pr.get("a_zero"),
+                            pr.get("w_gscale"), pr.get("a_gscale"), K, N, M)
         p = arr[i]
         p.M, p.N, p.K, p.wbits, p.abits = M, N, K, W.bits, A.bits
         p.W, p.A = W.struct(), A.struct()
-        p.scales = L.AptScales(ws_.data_ptr() if ws_ is not None else None, as_.data_ptr() if as_ is not None else None,
-                               None, None)
+        if sc is not None:
+            p.scales = sc
         p.kind, p.layout, p.out, p.ldo = kind, lay, out.data_ptr(), out.stride(0)
         outs.append(out)
     if workspace is None:

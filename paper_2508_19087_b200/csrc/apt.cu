@@ -425,6 +425,10 @@ size_t apt_gemm_zp_workspace_bytes(const apt_config* cfg, int32_t M, int32_t N, 
   return (apt_gemm_workspace_bytes(cfg, M, N, K) + 15) / 16 * 16 + (size_t)M * (size_t)N * 4u;
 }
 
+static apt_status grp_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, const apt_packed* W,
+                           const apt_packed* A, const apt_scales* scales, apt_out_kind kind, apt_layout layout,
+                           void* out, int64_t ldo, void* workspace, size_t ws_bytes, cudaStream_t s);
+
 apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, const apt_packed* W,
                     const apt_packed* A, const apt_scales* scales, apt_out_kind kind, apt_layout layout,
                     void* out, int64_t ldo, const apt_config* cfg, void* workspace, size_t ws_bytes,
@@ -442,7 +446,8 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
     return APT_ERR_INVALID_ARGUMENT;
   if (layout != APT_LAYOUT_ROW && layout != APT_LAYOUT_COL) return APT_ERR_INVALID_ARGUMENT;
   if (layout == APT_LAYOUT_ROW ? ldo < N : ldo < M) return APT_ERR_INVALID_ARGUMENT;
-  if (kind == APT_OUT_F16_SCALED && (!scales || !scales->w_scale)) return APT_ERR_INVALID_ARGUMENT;
+  if (kind == APT_OUT_F16_SCALED && (!scales || (!scales->w_scale && scales->group_size == 0)))
+    return APT_ERR_INVALID_ARGUMENT;
   if (!bound_ok(K, wbits, abits)) return APT_ERR_UNSUPPORTED;
   apt_config c;
   if (cfg) {
@@ -459,7 +464,22 @@ apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abit
   // zero points (NEXT-2): exact int32 Y into the workspace after the digit-expansion area, then the
   // elementwise zero-point epilogue
   const bool zp = kind == APT_OUT_F16_SCALED && (scales->w_zero || scales->a_zero);
-  const size_t y_off = (need0 + 15) / 16 * 16;
+  // group-wise scales (NEXT-2): the grouped kernel's signed-digit path, M in chunks of 16 tokens
+  if (scales && scales->group_size != 0) {
+    if (kind != APT_OUT_F16_SCALED || scales->group_size != 128 || !scales->w_gscale || zp) return APT_ERR_INVALID_ARGUMENT;
+    if (W->layout != APT_PACK_TILED || !A->digits || A->layout != APT_PACK_ROWS) return APT_ERR_UNSUPPORTED;
+    if (!workspace || ws_bytes < apt_gemm_grouped_workspace_bytes(1) || !aligned16(workspace)) return APT_ERR_WORKSPACE;
+    return grp_gemm(M, N, K, wbits, abits, W, A, scales, kind, layout, out, ldo, workspace, ws_bytes,
+                    reinterpret_cast<cudaStream_t>(stream));
+  }
+  // zero points at decode token counts: fused into the grouped kernel's epilogue (one launch, no int32 Y
+  // round trip) when the operands and the workspace allow it and no config was forced
+  if (zp && !cfg && M <= 16 && W->layout == APT_PACK_TILED && A->digits && A->layout == APT_PACK_ROWS && workspace &&
+      ws_bytes >= apt_gemm_grouped_workspace_bytes(1) && aligned16(workspace))
+    return grp_gemm(M, N, K, wbits, abits, W, A, scales, kind, layout, out, ldo, workspace, ws_bytes,
+                    reinterpret_cast<cudaStream_t>(stream));
+  // (never inside the ticket area, which every call leaves zero for the next one)
+  const size_t y_off = (std::max<size_t>(need0, APT_WS_TICKET_BYTES) + 15) / 16 * 16;
   const size_t need = zp ? y_off + (size_t)M * (size_t)N * 4u : need0;
   if (need > 0 && (!workspace || ws_bytes < need || !aligned16(workspace))) return APT_ERR_WORKSPACE;
   if (A->digits && !aligned16(A->digits)) return APT_ERR_INVALID_ARGUMENT;
@@ -612,16 +632,25 @@ size_t apt_gemm_grouped_workspace_bytes(int32_t count) {
   return APT_WS_TICKET_BYTES + (size_t)grp_max_workers() * 2u * 4u * 512u * 4u;
 }
 
-apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems, void* workspace, size_t ws_bytes,
-                            void* stream) {
+// The grouped launch behind apt_gemm_grouped and apt_gemm's group-scale / fused zero-point routes.
+// a_gs_ld[i] (nullable): leading dimension of problem i's a_gscale ([Kpad/128][a_gs_ld]); default its M.
+static apt_status grp_run(int32_t count, const apt_gemm_problem* problems, const int64_t* a_gs_ld, void* workspace,
+                          size_t ws_bytes, cudaStream_t stream) {
   if (count < 1 || count > APT_GROUP_MAX || count > apt::kGrpMax || !problems) return APT_ERR_INVALID_ARGUMENT;
   static_assert(APT_GROUP_MAX <= apt::kGrpMax, "group size");
-  apt::GrpArgs ga;
-  std::memset(&ga, 0, sizeof(ga));
+  static apt::GrpArgs ga_zero;  // zero-initialised template (the struct is ~19 KB)
+  apt::GrpArgs ga = ga_zero;
   int64_t blocks = 0, cost = 0;
   int wbmax = 1, cmax = 1;
+  const bool gs = problems[0].scales.group_size != 0;
   for (int i = 0; i < count; ++i) {
     const apt_gemm_problem& P = problems[i];
+    // group-wise scales (NEXT-2): fp16 output, groups of 128, the weights' [Kpad/128][N] scales required,
+    // no zero points, and all problems of a launch alike
+    if ((P.scales.group_size != 0) != gs) return APT_ERR_INVALID_ARGUMENT;
+    if (gs && (P.scales.group_size != 128 || P.kind != APT_OUT_F16_SCALED || !P.scales.w_gscale ||
+               P.scales.w_zero || P.scales.a_zero))
+      return APT_ERR_INVALID_ARGUMENT;
     const int32_t M = P.M, N = P.N, K = P.K;
     if (M <= 0 || M > 16 || N <= 0 || K <= 0 || P.wbits < 1 || P.wbits > 8 || P.abits < 1 || P.abits > 8 || !P.out)
       return APT_ERR_INVALID_ARGUMENT;
@@ -633,8 +662,7 @@ apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems, voi
       return APT_ERR_INVALID_ARGUMENT;
     if (P.layout != APT_LAYOUT_ROW && P.layout != APT_LAYOUT_COL) return APT_ERR_INVALID_ARGUMENT;
     if (P.layout == APT_LAYOUT_ROW ? P.ldo < N : P.ldo < M) return APT_ERR_INVALID_ARGUMENT;
-    if (P.kind == APT_OUT_F16_SCALED && !P.scales.w_scale) return APT_ERR_INVALID_ARGUMENT;
-    if (P.scales.w_zero || P.scales.a_zero) return APT_ERR_INVALID_ARGUMENT;
+    if (P.kind == APT_OUT_F16_SCALED && !gs && !P.scales.w_scale) return APT_ERR_INVALID_ARGUMENT;
     if (!bound_ok(K, P.wbits, P.abits)) return APT_ERR_UNSUPPORTED;
     if (kpad_of(K) * 255ll * 255ll >= (1ll << 32)) return APT_ERR_UNSUPPORTED;  // u * 2^s digits (gemm_dec.cu)
     apt::GrpProblem& q = ga.p[i];
@@ -669,6 +697,11 @@ apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems, voi
     e.kpad = (int32_t)kpad_of(K);
     e.h_w = 1 << (P.wbits - 1);
     e.h_a = 1 << (P.abits - 1);
+    q.w_zero = P.kind == APT_OUT_F16_SCALED ? P.scales.w_zero : nullptr;
+    q.a_zero = P.kind == APT_OUT_F16_SCALED ? P.scales.a_zero : nullptr;
+    q.w_gs = gs ? P.scales.w_gscale : nullptr;
+    q.a_gs = gs ? P.scales.a_gscale : nullptr;
+    q.a_gs_ld = a_gs_ld ? a_gs_ld[i] : M;
     q.k_words = P.W.k_words;
     q.nb = P.W.k_words / 8;  // units of 128 rows x 256 K per 128-row tile
     q.tiles = (N + 127) / 128;
@@ -685,7 +718,7 @@ apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems, voi
 #ifdef APT_GRP_CPS
   const int cps = APT_GRP_CPS;
 #else
-  const int cps = apt::grp_ctas_per_sm(wbmax);
+  const int cps = apt::grp_ctas_per_sm(wbmax, gs);
 #endif
   int64_t workers = std::min<int64_t>((int64_t)device_sms() * cps, cost / cmax);
   workers = std::max<int64_t>(workers, 1);
@@ -698,8 +731,58 @@ apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems, voi
   ga.total_cost = cost;
   ga.tickets = reinterpret_cast<uint32_t*>(workspace);
   ga.partials = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(workspace) + APT_WS_TICKET_BYTES);
-  cudaError_t err = apt::launch_gemm_grp(ga, wbmax, (int)workers, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t err = apt::launch_gemm_grp(ga, wbmax, (int)workers, gs, stream);
   return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+}
+
+apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems, void* workspace, size_t ws_bytes,
+                            void* stream) {
+  return grp_run(count, problems, nullptr, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// apt_gemm through the grouped kernel: the M tokens in chunks of at most 16 rows, each chunk one problem
+// (A, its row sums, scales, zero points and group scales offset to the chunk; the output offset to its
+// rows / columns), up to APT_GROUP_MAX chunks per launch
+static apt_status grp_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int32_t abits, const apt_packed* W,
+                           const apt_packed* A, const apt_scales* scales, apt_out_kind kind, apt_layout layout,
+                           void* out, int64_t ldo, void* workspace, size_t ws_bytes, cudaStream_t s) {
+  const int esz = kind == APT_OUT_F16_SCALED ? 2 : 4;
+  const int64_t kp = kpad_of(K);
+  apt_gemm_problem pr[APT_GROUP_MAX];
+  int64_t ld[APT_GROUP_MAX];
+  int n = 0;
+  for (int32_t m0 = 0; m0 < M; m0 += 16) {
+    apt_gemm_problem& P = pr[n];
+    std::memset(&P, 0, sizeof(P));
+    const int32_t mc = std::min(16, M - m0);
+    P.M = mc;
+    P.N = N;
+    P.K = K;
+    P.wbits = wbits;
+    P.abits = abits;
+    P.W = *W;
+    P.A = *A;
+    P.A.rows = mc;
+    P.A.row_sum = A->row_sum + m0;
+    P.A.digits = A->digits + (int64_t)m0 * kp;
+    if (scales) {
+      P.scales = *scales;
+      if (scales->a_scale) P.scales.a_scale = scales->a_scale + m0;
+      if (scales->a_zero) P.scales.a_zero = scales->a_zero + m0;
+      if (scales->a_gscale) P.scales.a_gscale = scales->a_gscale + m0;
+    }
+    P.kind = kind;
+    P.layout = layout;
+    P.out = reinterpret_cast<uint8_t*>(out) + (layout == APT_LAYOUT_ROW ? (int64_t)m0 * ldo : (int64_t)m0) * esz;
+    P.ldo = ldo;
+    ld[n] = M;
+    if (++n == APT_GROUP_MAX || m0 + 16 >= M) {
+      const apt_status st = grp_run(n, pr, ld, workspace, ws_bytes, s);
+      if (st != APT_OK) return st;
+      n = 0;
+    }
+  }
+  return APT_OK;
 }
 
 apt_status apt_recombine_plane_products(const int32_t* parts, int32_t abits, int32_t wbits, int64_t part_stride,

@@ -28,10 +28,12 @@ __global__ void __launch_bounds__(256) zp_epilogue_kernel(ZpArgs p) {
     const float as = p.a_scale ? __ldg(p.a_scale + m) : 1.f;
     const float az = p.a_zero ? __ldg(p.a_zero + m) : 0.f;
     const float wz = p.w_zero ? __ldg(p.w_zero + n) : 0.f;
-    float v = ((float)__ldg(p.y + i) * ws) * as;
-    v += ((float)__ldg(p.w_rowsum + n) * ws) * az;
-    v += ((float)__ldg(p.a_rowsum + m) * as) * wz;
-    v += ((float)p.K * az) * wz;
+    // every product and sum rounded on its own (no FMA contraction): the documented fp32 order, and the
+    // same bits as the grouped kernel's fused zero-point epilogue
+    float v = __fmul_rn(__fmul_rn((float)__ldg(p.y + i), ws), as);
+    v = __fadd_rn(v, __fmul_rn(__fmul_rn((float)__ldg(p.w_rowsum + n), ws), az));
+    v = __fadd_rn(v, __fmul_rn(__fmul_rn((float)__ldg(p.a_rowsum + m), as), wz));
+    v = __fadd_rn(v, __fmul_rn(__fmul_rn((float)p.K, az), wz));
     const int64_t off = p.layout == 0 ? (int64_t)m * p.ldo + n : (int64_t)n * p.ldo + m;
     p.out[off] = __float2half_rn(v);
   }

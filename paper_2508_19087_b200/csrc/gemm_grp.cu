@@ -66,6 +66,34 @@ __device__ __forceinline__ void grp_mma(int (&c)[4], uint32_t a0, uint32_t a1, u
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void grp_mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                           uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+template <bool S>
+__device__ __forceinline__ void grp_mma_x(int* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                          uint32_t b1) {
+  if constexpr (S) grp_mma_s8(*reinterpret_cast<int(*)[4]>(c), a0, a1, a2, a3, b0, b1);
+  else grp_mma(*reinterpret_cast<int(*)[4]>(c), a0, a1, a2, a3, b0, b1);
+}
+
+// Group-wise scales need every 128-element group's product on its own, so the digits become SIGNED
+// (x * 2^s as int8: no rank-1 row-sum terms per group): bytewise d - h 2^s without borrows between bytes.
+// Weight digits: top-aligned (W1, W2: u 2^(8-W); W4: u 16) and W8 -> flip bit 7; W3 (u 16 < 128) and
+// W5-W7 (u < 2^W) -> ((d | 0x80) - h 2^s) ^ 0x80.
+template <int WB>
+__device__ __forceinline__ uint32_t grp_signed_w(uint32_t d) {
+  if constexpr (WB <= 2 || WB == 4 || WB == 8) return d ^ 0x80808080u;
+  else if constexpr (WB == 3) return ((d | 0x80808080u) - 0x40404040u) ^ 0x80808080u;
+  else return ((d | 0x80808080u) - (1u << (WB - 1)) * 0x01010101u) ^ 0x80808080u;
+}
+// token digits u (low bits) -> signed codes x = u - h_a (hA = h_a * 0x01010101; h_a = 128 flips bit 7)
+__device__ __forceinline__ uint32_t grp_signed_a(uint32_t u, uint32_t hA, bool ab8) {
+  return ab8 ? u ^ 0x80808080u : ((u | 0x80808080u) - hA) ^ 0x80808080u;
+}
+
 // worker owning block i of problem q (midpoint rule): floor((2 cost0 + (2 i + 1) cost) * W / (2 T))
 __device__ __forceinline__ int grp_owner(const GrpArgs& a, const GrpProblem& q, int64_t i) {
   return (int)((2 * q.cost0 + (2 * i + 1) * (int64_t)q.cost) * a.workers / (2 * a.total_cost));
@@ -95,14 +123,22 @@ __device__ void grp_find(const GrpArgs& a, int w, int& p_out, int64_t& i_out, in
 }
 
 __device__ __forceinline__ void grp_store(const EpilogueArgs& e, int m, int n, uint32_t acc, int shift, int32_t ra,
-                                          int32_t rw, float wsc, float as) {
+                                          int32_t rw, float wsc, float as, float az = 0.f, float wz = 0.f,
+                                          bool zp = false) {
   // acc = U * 2^shift; Y = U - h_w RA - h_a RW - Kpad h_a h_w (mod 2^32, exact: reading Q8)
   const uint32_t y = (acc >> shift) - (uint32_t)e.h_w * (uint32_t)ra - (uint32_t)e.h_a * (uint32_t)rw -
                      (uint32_t)e.kpad * (uint32_t)e.h_a * (uint32_t)e.h_w;
   if (m >= e.M || n >= e.N) return;
   const int64_t off = e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m;
   if (e.kind == 2) {
-    const float v = ((float)(int32_t)y * wsc) * as;
+    float v = ((float)(int32_t)y * wsc) * as;
+    if (zp) {  // zero points (P:199-201 on both operands): the apt_gemm zero-point formula, every operation
+               // rounded on its own as in epilogue_zp.cu (bit-identical results)
+      v = __fmul_rn(__fmul_rn((float)(int32_t)y, wsc), as);
+      v = __fadd_rn(v, __fmul_rn(__fmul_rn((float)rw, wsc), az));
+      v = __fadd_rn(v, __fmul_rn(__fmul_rn((float)ra, as), wz));
+      v = __fadd_rn(v, __fmul_rn(__fmul_rn((float)e.K, az), wz));
+    }
     unsigned short hv;
     asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hv) : "f"(v));
     reinterpret_cast<unsigned short*>(e.out)[off] = hv;
@@ -127,8 +163,8 @@ __device__ __forceinline__ void grp_wait(uint32_t bar, uint32_t parity) {
 #endif
 }
 
-template <int WBMAX, bool MT1>
-__global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant__ GrpArgs a) {
+template <int WBMAX, bool MT1, bool GS>
+__global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_constant__ GrpArgs a) {
   using SH = GrpShape<WBMAX>;
   constexpr int D = SH::kD;
   extern __shared__ __align__(1024) uint8_t smem[];  // no static shared memory: the swizzled token
@@ -261,12 +297,38 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
     int acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = 0;
+    // group-wise scales (GS): fp32 sums of the groups' scaled exact products (acc unused)
+    float facc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) facc[j] = 0.f;
+    const uint32_t hA = (uint32_t)q.e.h_a * 0x01010101u;
+    const bool ab8 = q.e.h_a == 128;
 
     auto run = [&](auto wbc, auto mtc) {
       constexpr int WB = decltype(wbc)::value;
       constexpr int MT = decltype(mtc)::value;
+      const int shift = grp_shift(WB);
 #pragma unroll 1
       for (int b = 0; b < seg; ++b) {
+        // GS: this block's two groups' scales (rows / tokens of the lane), requested before the wait
+        [[maybe_unused]] float sw[2][8], sa[2][2];
+        if constexpr (GS) {
+          const int64_t g0 = 2 * (int64_t)(b_in + b);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              // MT 2: row n_w + 8 (j >> 1) + 2t + (j & 1); MT 1: row n_w + 16 (j >> 1) + g + 8 (j & 1) (j < 4)
+              const int n = MT == 2 ? n_w + 8 * (j >> 1) + 2 * t + (j & 1) : n_w + 16 * (j >> 1) + g + 8 * (j & 1);
+              sw[c][j] = (MT == 2 || j < 4) ? __ldg(q.w_gs + (g0 + c) * q.e.N + min(n, q.e.N - 1)) : 0.f;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int m = min(MT == 2 ? g + 8 * h : 2 * t + h, q.e.M - 1);
+              sa[c][h] = q.a_gs ? __ldg(q.a_gs + (g0 + c) * q.a_gs_ld + m) : (q.e.a_scale ? __ldg(q.e.a_scale + m) : 1.f);
+            }
+          }
+        }
         grp_wait(full(slot), ph & 1);
         const uint32_t sl = sbase + (uint32_t)(slot * SH::kSlot);
         uint4 tk0[4], tk1[4];  // [2 box + k]: word t (box 0) then word t + 4 (box 1), rows g / g + 8
@@ -278,6 +340,22 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
           if (MT == 2)
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(tk1[j].x), "=r"(tk1[j].y), "=r"(tk1[j].z), "=r"(tk1[j].w)
                          : "r"(sl + trow1 + ch));
+          if constexpr (GS) {
+            uint32_t* t0 = reinterpret_cast<uint32_t*>(&tk0[j]);
+            uint32_t* t1 = reinterpret_cast<uint32_t*>(&tk1[j]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              t0[e] = grp_signed_a(t0[e], hA, ab8);
+              if (MT == 2) t1[e] = grp_signed_a(t1[e], hA, ab8);
+            }
+          }
+        }
+        int ai[2][16];  // GS: the block's per-group int products (c = group half)
+        if constexpr (GS) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) ai[c][j] = 0;
         }
         if constexpr (MT == 2) {
           // weights = B operand (8 rows per MMA), tokens g, g + 8 = A operand: acc[4 qq + j]
@@ -295,12 +373,16 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
 #pragma unroll
               for (int i = 0; i < WB; ++i) wr[i] = c ? wv[i].y : wv[i].x;
               grp_rebuild<WB>(wr, o);
+              if constexpr (GS) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] = grp_signed_w<WB>(o[j]);
+              }
               const uint32_t* ag = reinterpret_cast<const uint32_t*>(&tk0[2 * c]);
               const uint32_t* ah = reinterpret_cast<const uint32_t*>(&tk1[2 * c]);
+              int* d = GS ? &ai[c][4 * qq] : &acc[4 * qq];
 #pragma unroll
               for (int s4 = 0; s4 < 4; ++s4)
-                grp_mma(*reinterpret_cast<int(*)[4]>(acc + 4 * qq), ag[2 * s4], ah[2 * s4], ag[2 * s4 + 1], ah[2 * s4 + 1],
-                        o[2 * s4], o[2 * s4 + 1]);
+                grp_mma_x<GS>(d, ag[2 * s4], ah[2 * s4], ag[2 * s4 + 1], ah[2 * s4 + 1], o[2 * s4], o[2 * s4 + 1]);
             }
           }
         } else {
@@ -311,11 +393,11 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
             uint2 wg[WB], wh[WB];
 #pragma unroll
             for (int i = 0; i < WB; ++i) {
-              const uint32_t b = sl + woff + (uint32_t)(i * 4096 + P * 256);
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wg[i].x) : "r"(b));
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wg[i].y) : "r"(b + 2048));
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wh[i].x) : "r"(b + 128));
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wh[i].y) : "r"(b + 2048 + 128));
+              const uint32_t bb = sl + woff + (uint32_t)(i * 4096 + P * 256);
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wg[i].x) : "r"(bb));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wg[i].y) : "r"(bb + 2048));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wh[i].x) : "r"(bb + 128));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wh[i].y) : "r"(bb + 2048 + 128));
             }
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -327,11 +409,18 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
               }
               grp_rebuild<WB>(xg, og);
               grp_rebuild<WB>(xh, oh);
+              if constexpr (GS) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  og[j] = grp_signed_w<WB>(og[j]);
+                  oh[j] = grp_signed_w<WB>(oh[j]);
+                }
+              }
               const uint32_t* ag = reinterpret_cast<const uint32_t*>(&tk0[2 * c]);
+              int* d = GS ? &ai[c][4 * P] : &acc[4 * P];
 #pragma unroll
               for (int s4 = 0; s4 < 4; ++s4)
-                grp_mma(*reinterpret_cast<int(*)[4]>(acc + 4 * P), og[2 * s4], oh[2 * s4], og[2 * s4 + 1], oh[2 * s4 + 1],
-                        ag[2 * s4], ag[2 * s4 + 1]);
+                grp_mma_x<GS>(d, og[2 * s4], oh[2 * s4], og[2 * s4 + 1], oh[2 * s4 + 1], ag[2 * s4], ag[2 * s4 + 1]);
             }
           }
         }
@@ -344,6 +433,20 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
         if (++slot == D) {
           slot = 0;
           ++ph;
+        }
+        if constexpr (GS) {
+          // fold the two groups: facc += ((float) Y_g * w_gscale) * a_gscale (Y_g exact: the int products
+          // of signed digits, weights scaled by 2^shift)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int j = 0; j < (MT == 2 ? 16 : 8); ++j) {
+              // MT 2: j = 4 qq + 2 h + cc (row 8 qq + 2t + cc, token g + 8h); MT 1: j = 4 P + 2 h + cc (row
+              // 16 P + g + 8h, token 2t + cc)
+              const float w_s = MT == 2 ? sw[c][2 * (j >> 2) + (j & 1)] : sw[c][2 * (j >> 2) + ((j >> 1) & 1)];
+              const float a_s = MT == 2 ? sa[c][(j >> 1) & 1] : sa[c][j & 1];
+              facc[j] += ((float)(ai[c][j] >> shift) * w_s) * a_s;
+            }
         }
       }
       return 0;
@@ -368,6 +471,10 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
       run_w(std::integral_constant<int, 2>{});
     }
     const int shift = grp_shift(q.wbits);
+    if constexpr (GS) {  // the split-tile exchange below moves the fp32 sums as their bit patterns
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = __float_as_int(facc[j]);
+    }
 
     // ---- the tile: whole (one CTA) or split (partials + ticket; the last CTA to arrive reduces)
     const int64_t tfirst = (int64_t)tile * nb;
@@ -396,21 +503,39 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
           if (o == w) continue;
           const int* po = a.partials + (((int64_t)o * 2 + (o == fw ? 1 : 0)) * 4 + cw) * 512;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] += __ldcg(po + j * 32 + lane);
+          for (int j = 0; j < 16; ++j) {
+            const int v = __ldcg(po + j * 32 + lane);
+            acc[j] = GS ? __float_as_int(__int_as_float(acc[j]) + __int_as_float(v)) : acc[j] + v;
+          }
         }
       }
     }
-    if (epi) {
+    if (epi && GS) {
+      // group-wise scales: out = RN_fp16(sum_g ((float) Y_g * w_gscale) * a_gscale), fp16 row / column layout
+      const EpilogueArgs& e = q.e;
+      unsigned short* out = reinterpret_cast<unsigned short*>(e.out);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int m = narrow ? 2 * t + (j & 1) : g + 8 * ((j >> 1) & 1);
+        const int n = narrow ? n_w + 16 * (j >> 2) + g + 8 * ((j >> 1) & 1) : n_w + 8 * (j >> 2) + 2 * t + (j & 1);
+        if ((narrow && j >= 8) || m >= e.M || n >= e.N) continue;
+        unsigned short hv;
+        asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hv) : "f"(__int_as_float(acc[j])));
+        out[e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m] = hv;
+      }
+    } else if (epi) {
       const EpilogueArgs& e = q.e;
       const bool f16 = e.kind == 2;
+      const bool zp = f16 && (q.w_zero || q.a_zero);
       if (!narrow) {  // acc[4 qq + 2 h + c]: token g + 8h, weight row n_w + 8 qq + 2t + c
         int32_t ra[2];
-        float as[2];
+        float as[2], az[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int m = min(g + 8 * h, e.M - 1);
           ra[h] = __ldg(e.a_rowsum + m);
           as[h] = (f16 && e.a_scale) ? __ldg(e.a_scale + m) : 1.f;
+          az[h] = (zp && q.a_zero) ? __ldg(q.a_zero + m) : 0.f;
         }
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq)
@@ -419,18 +544,20 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
             const int n = n_w + 8 * qq + 2 * t + c, nc = min(n, e.N - 1);
             const int32_t rw = __ldg(e.w_rowsum + nc);
             const float wsc = f16 ? __ldg(e.w_scale + nc) : 0.f;
+            const float wz = (zp && q.w_zero) ? __ldg(q.w_zero + nc) : 0.f;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              grp_store(e, g + 8 * h, n, (uint32_t)acc[4 * qq + 2 * h + c], shift, ra[h], rw, wsc, as[h]);
+              grp_store(e, g + 8 * h, n, (uint32_t)acc[4 * qq + 2 * h + c], shift, ra[h], rw, wsc, as[h], az[h], wz, zp);
           }
       } else {  // acc[4 P + 2 h + c]: weight row n_w + 16 P + g + 8 h, token 2t + c
         int32_t ra[2];
-        float as[2];
+        float as[2], az[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int m = min(2 * t + c, e.M - 1);
           ra[c] = __ldg(e.a_rowsum + m);
           as[c] = (f16 && e.a_scale) ? __ldg(e.a_scale + m) : 1.f;
+          az[c] = (zp && q.a_zero) ? __ldg(q.a_zero + m) : 0.f;
         }
 #pragma unroll
         for (int P = 0; P < 2; ++P)
@@ -439,9 +566,10 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
             const int n = n_w + 16 * P + g + 8 * h, nc = min(n, e.N - 1);
             const int32_t rw = __ldg(e.w_rowsum + nc);
             const float wsc = f16 ? __ldg(e.w_scale + nc) : 0.f;
+            const float wz = (zp && q.w_zero) ? __ldg(q.w_zero + nc) : 0.f;
 #pragma unroll
             for (int c = 0; c < 2; ++c)
-              grp_store(e, 2 * t + c, n, (uint32_t)acc[4 * P + 2 * h + c], shift, ra[c], rw, wsc, as[c]);
+              grp_store(e, 2 * t + c, n, (uint32_t)acc[4 * P + 2 * h + c], shift, ra[c], rw, wsc, as[c], az[c], wz, zp);
           }
       }
     }
@@ -454,26 +582,29 @@ __global__ void __launch_bounds__(160, 3) gemm_grp_kernel(const __grid_constant_
   }
 }
 
-template <int WBMAX, bool MT1>
+template <int WBMAX, bool MT1, bool GS>
 static cudaError_t launch_grp2(const GrpArgs& a, int ctas, cudaStream_t stream) {
   constexpr int kSmem = GrpShape<WBMAX>::kSmem;
-  cudaError_t err = set_smem_once<gemm_grp_kernel<WBMAX, MT1>>(kSmem);
+  cudaError_t err = set_smem_once<gemm_grp_kernel<WBMAX, MT1, GS>>(kSmem);
   if (err != cudaSuccess) return err;
-  return launch_pdl(gemm_grp_kernel<WBMAX, MT1>, dim3(ctas), dim3(160), kSmem, stream, dim3(1, 1, 1), a);
+  return launch_pdl(gemm_grp_kernel<WBMAX, MT1, GS>, dim3(ctas), dim3(160), kSmem, stream, dim3(1, 1, 1), a);
 }
 
 int grp_wbmax_class(int wbmax) { return wbmax <= 2 ? 2 : wbmax <= 4 ? 4 : 8; }
 // CTAs per SM (shared memory: 3 x 72 KB at WBMAX 2, 3 x 60 KB at WBMAX 4, 2 x 108 KB at WBMAX 8)
-int grp_ctas_per_sm(int wbmax) { return grp_wbmax_class(wbmax) <= 4 ? 3 : 2; }
+int grp_ctas_per_sm(int wbmax, bool gs) { return gs ? 2 : grp_wbmax_class(wbmax) <= 4 ? 3 : 2; }
 
 #ifndef APT_GRP_MT1
 #define APT_GRP_MT1 true
 #endif
-cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, cudaStream_t stream) {
-  switch (grp_wbmax_class(wbmax)) {
-    case 2: return launch_grp2<2, APT_GRP_MT1>(a, ctas, stream);
-    case 4: return launch_grp2<4, APT_GRP_MT1>(a, ctas, stream);
-    default: return launch_grp2<8, APT_GRP_MT1>(a, ctas, stream);
+cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, cudaStream_t stream) {
+  switch (grp_wbmax_class(wbmax) * 2 + (gs ? 1 : 0)) {
+    case 4: return launch_grp2<2, APT_GRP_MT1, false>(a, ctas, stream);
+    case 5: return launch_grp2<2, APT_GRP_MT1, true>(a, ctas, stream);
+    case 8: return launch_grp2<4, APT_GRP_MT1, false>(a, ctas, stream);
+    case 9: return launch_grp2<4, APT_GRP_MT1, true>(a, ctas, stream);
+    case 17: return launch_grp2<8, APT_GRP_MT1, true>(a, ctas, stream);
+    default: return launch_grp2<8, APT_GRP_MT1, false>(a, ctas, stream);
   }
 }
 

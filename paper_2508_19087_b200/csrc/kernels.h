@@ -127,6 +127,11 @@ struct GrpProblem {
   EpilogueArgs e;
   int64_t blk0;            // global index of the problem's first block (tile-major, then K)
   int64_t cost0;           // total cost of the blocks before the problem
+  const float* w_zero;     // zero points [N] / [M] (fp16 output), nullable
+  const float* a_zero;
+  const float* w_gs;       // group-wise (128) scales [Kpad / 128][N] (GS launches), else null
+  const float* a_gs;       // [Kpad / 128][a_gs_ld], nullable (then a_scale per token)
+  int64_t a_gs_ld;
   int32_t k_words, nb, tiles, wbits, cost;  // nb = Kpad / 256 blocks per row tile; tiles = ceil(N / 128)
 };
 struct GrpArgs {
@@ -137,6 +142,6 @@ struct GrpArgs {
   GrpProblem p[kGrpMax];
 };
 int grp_wbmax_class(int wbmax);
-int grp_ctas_per_sm(int wbmax);
-cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, cudaStream_t stream);
+int grp_ctas_per_sm(int wbmax, bool gs);
+cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, cudaStream_t stream);
 }  // namespace apt

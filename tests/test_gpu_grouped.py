@@ -245,3 +245,112 @@ def test_pack_grouped_rejects():
     big = _dev(signed_codes(65, 256, 2, seed=2))  # more rows than the one-word-per-thread pack takes
     with pytest.raises(P._lib.AptError):
         P.pack_grouped([dict(codes=big, bits=2, out=P.alloc_packed(65, 256, 2, DEV, digits=True))])
+
+
+# ----------------------------------------------------------------------------- NEXT-2: group scales, fused zero points
+
+def _gs_problem(m, n, k, pw, pa, seed, a_groups=True, layout="row"):
+    a = signed_codes(m, k, pa, seed=seed)
+    w = signed_codes(n, k, pw, seed=seed + 1)
+    G = O.kpad(k) // 128
+    rng = np.random.default_rng(seed)
+    wg = np.exp2(rng.uniform(-10, -6, (G, n))).astype(np.float32)
+    ag = np.exp2(rng.uniform(-6, -2, (G, m))).astype(np.float32) if a_groups else None
+    sa = np.exp2(rng.uniform(-6, -2, m)).astype(np.float32)
+    pr = dict(W=P.pack(_dev(w), pw, tiled=True), A=P.pack(_dev(a), pa, digits=True), out_kind="f16", layout=layout,
+              w_gscale=_dev(wg))
+    if a_groups:
+        pr["a_gscale"] = _dev(ag)
+    else:
+        pr["a_scale"] = _dev(sa)
+    return pr, (a, w, wg, ag, sa)
+
+
+def _gs_check(got, a, w, wg, ag, sa, layout="row"):
+    """Reading R-G: fp32 sums of the groups' exactly computed products, one fp16 rounding; bound
+    2^-11 |ref| (the rounding) + 2^-16 sum_g |Y_g s_w s_a| (fp32 accumulation over <= 256 groups) + 2^-24."""
+    got = got.cpu().numpy().astype(np.float64)
+    if layout == "col":
+        got = got.T
+    ref = O.group_dequant_gemm_fp64(a, w, wg, ag, None if ag is not None else sa)
+    k = a.shape[1]
+    mag = np.zeros_like(ref)
+    for g in range(-(-k // 128)):
+        yg = np.abs(O.gemm_signed(a[:, 128 * g:128 * g + 128], w[:, 128 * g:128 * g + 128]).astype(np.float64))
+        s_a = ag[g].astype(np.float64) if ag is not None else sa.astype(np.float64)
+        mag += yg * wg[g].astype(np.float64)[None, :] * s_a[:, None]
+    assert (np.abs(got - ref) <= 2.0 ** -11 * np.abs(ref) + 2.0 ** -16 * mag + 2.0 ** -24).all()
+
+
+@pytest.mark.parametrize("wmax", [2, 4, 8])
+def test_group_scales_grouped(wmax):
+    """apt_gemm_grouped with group-wise (128) scales on ragged problems of every width up to wmax, with and
+    without activation group scales, both layouts, vs oracle.group_dequant_gemm_fp64."""
+    rng = np.random.default_rng(40 + wmax)
+    cases = [(int(rng.integers(1, 17)), int(rng.integers(1, 300)), int(rng.integers(1, 2000)),
+              int(rng.integers(1, wmax + 1)) if i else wmax, int(rng.integers(1, 9))) for i in range(9)]
+    prs, refs = [], []
+    for i, c in enumerate(cases):
+        pr, ref = _gs_problem(*c, seed=1200 + 17 * i, a_groups=bool(i % 2), layout="col" if i % 3 == 0 else "row")
+        prs.append(pr)
+        refs.append((ref, pr["layout"]))
+    outs = P.gemm_grouped(prs)
+    for out, (ref, lay) in zip(outs, refs):
+        _gs_check(out, *ref, layout=lay)
+    _tickets_zero()
+
+
+@pytest.mark.parametrize("m", [1, 8, 16, 17, 100, 1030])
+def test_group_scales_apt_gemm_any_m(m):
+    """apt_gemm with group scales at any token count (chunks of 16 tokens, several grouped launches for
+    m > 1024), Llama-like K = 4096 with K = 11008's ragged group count exercised at small m."""
+    k = 11008 if m <= 16 else 4096
+    n = 4096 if m <= 16 else 384
+    pr, ref = _gs_problem(m, n, k, 4, 4, seed=77 + m, a_groups=m % 2 == 0)
+    got = P.gemm(pr["W"], pr["A"], out_kind="f16", w_gscale=pr["w_gscale"], a_gscale=pr.get("a_gscale"),
+                 a_scale=pr.get("a_scale"))
+    _gs_check(got, *ref)
+    _tickets_zero()
+
+
+def test_group_scales_llama7b_decode_bench_shapes():
+    """Group scales (W4A4, 128-groups on both operands, the Atom-128G configuration) at the 9 decode shapes
+    of BASELINE configs[1] in one grouped launch, every output element vs the fp64 oracle."""
+    prs, refs = [], []
+    for (n, k) in LLAMA7B:
+        for m in (1, 8, 16):
+            pr, ref = _gs_problem(m, n, k, 4, 4, seed=n + k + m)
+            prs.append(pr)
+            refs.append(ref)
+    for out, ref in zip(P.gemm_grouped(prs), refs):
+        _gs_check(out, *ref)
+
+
+@pytest.mark.parametrize("m", [1, 5, 16])
+def test_zero_points_fused_decode(m):
+    """Zero points at decode token counts go through the grouped kernel's epilogue (one launch); the
+    result is bit-identical to the two-pass int32-Y route (forced by passing a config) and within the
+    zero-point bound of the fp64 dequantize-then-multiply oracle."""
+    n, k, pa, pw = 4096, 4096, 4, 3
+    a = signed_codes(m, k, pa, seed=60 + m)
+    w = signed_codes(n, k, pw, seed=61)
+    rng = np.random.default_rng(m)
+    ws = log_uniform_scales(n, -10, -6, seed=7)
+    as_ = log_uniform_scales(m, -6, -2, seed=8)
+    wz = (rng.uniform(-1, 1, n) * 2.0 ** -8).astype(np.float32)
+    az = (rng.uniform(-1, 1, m) * 2.0 ** -3).astype(np.float32)
+    A = P.pack(_dev(a), pa, digits=True)
+    W = P.pack(_dev(w), pw, tiled=True)
+    kw = dict(out_kind="f16", w_scale=_dev(ws), a_scale=_dev(as_), w_zero=_dev(wz), a_zero=_dev(az))
+    fused = P.gemm(W, A, **kw)
+    two_pass = P.gemm(W, A, config=P.select_config(m, n, k, pw, pa), **kw)
+    assert torch.equal(fused.view(torch.int16), two_pass.view(torch.int16))
+    ref = O.dequant_gemm_fp64(a, w, ws, as_, wz, az)
+    y = O.gemm_signed(a, w).astype(np.float64)
+    ra, rw = a.astype(np.float64).sum(1), w.astype(np.float64).sum(1)
+    mag = (np.abs(y * ws[None, :] * as_[:, None]) + np.abs(rw[None, :] * ws[None, :] * az[:, None]) +
+           np.abs(ra[:, None] * as_[:, None] * wz[None, :]) + np.abs(k * az[:, None] * wz[None, :]))
+    assert (np.abs(fused.cpu().numpy().astype(np.float64) - ref) <= 1e-3 * mag + 2.0 ** -24).all()
+    # the same problem inside a group with others
+    outs = P.gemm_grouped([dict(W=W, A=A, **kw), _problem(16, 300, 700, 2, 2, seed=5, kind="f16")[0]])
+    assert torch.equal(outs[0].view(torch.int16), fused.view(torch.int16))
