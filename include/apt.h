@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define APT_ABI_VERSION 7
+#define APT_ABI_VERSION 8
 #define APT_KPAD_QUANTUM 256 /* packed rows are padded to Kpad = round_up(K, 256) elements */
 #define APT_GROUP_MAX 64     /* problems per grouped call (apt_pack_grouped, apt_gemm_grouped) */
 
@@ -367,6 +367,13 @@ APT_API apt_status apt_gemm(int32_t M, int32_t N, int32_t K, int32_t wbits, int3
  *               workspace serves both kinds of call on one stream).
  * Errors: APT_ERR_INVALID_ARGUMENT (count outside [1, APT_GROUP_MAX], a problem violating the above),
  *         APT_ERR_UNSUPPORTED (int32 bound), APT_ERR_WORKSPACE, APT_ERR_CUDA. */
+/* Epilogue-direct peer stores (SURVEY §8f NEXT-4 ii): every output element is also written, at the same
+ * byte offset, to out_peers[0 .. n_peers-1] (device pointers valid on the calling device, e.g. NVLink
+ * peer mappings of a symmetric-memory buffer).  With out pointing at a rank's own slice of a gathered
+ * tensor parallel output, the GEMM itself is the all-gather: no staging copy, no collective launch.  The
+ * stores are plain weak global stores; the caller makes them visible to the peers (e.g. a symmetric-
+ * memory barrier after the call, stream-ordered). */
+#define APT_MAX_PEERS 7
 typedef struct {
   int32_t M, N, K, wbits, abits;
   apt_packed W;
@@ -376,6 +383,8 @@ typedef struct {
   int32_t layout; /* apt_layout   */
   void* out;
   int64_t ldo;
+  void* out_peers[APT_MAX_PEERS];
+  int32_t n_peers; /* 0 .. APT_MAX_PEERS */
 } apt_gemm_problem;
 APT_API size_t apt_gemm_grouped_workspace_bytes(int32_t count);
 APT_API apt_status apt_gemm_grouped(int32_t count, const apt_gemm_problem* problems /* host */, void* workspace,

@@ -16,7 +16,7 @@ APT_OUT_I32_SIGNED, APT_OUT_I32_BIPOLAR, APT_OUT_F16_SCALED = 0, 1, 2
 APT_LAYOUT_ROW, APT_LAYOUT_COL = 0, 1
 APT_KERNEL_AUTO, APT_KERNEL_TC, APT_KERNEL_GEMV, APT_KERNEL_SKINNY, APT_KERNEL_DEC, APT_KERNEL_PF = 0, 2, 3, 4, 5, 6
 APT_MMA_I8, APT_MMA_MXF4 = 0, 1
-ABI_VERSION = 7  # include/apt.h APT_ABI_VERSION this binding marshals for
+ABI_VERSION = 8  # include/apt.h APT_ABI_VERSION this binding marshals for
 APT_PACK_ROWS, APT_PACK_TILED = 0, 1
 
 EXPORTED = ["apt_packed_plane_bytes", "apt_pack_bipolar", "apt_quantize_pack", "apt_select_config", "apt_gemm_workspace_bytes", "apt_gemm_zp_workspace_bytes",
@@ -40,10 +40,12 @@ class AptScales(ctypes.Structure):
 class AptGemmProblem(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("wbits", ctypes.c_int32),
                 ("abits", ctypes.c_int32), ("W", AptPacked), ("A", AptPacked), ("scales", AptScales),
-                ("kind", ctypes.c_int32), ("layout", ctypes.c_int32), ("out", ctypes.c_void_p), ("ldo", ctypes.c_int64)]
+                ("kind", ctypes.c_int32), ("layout", ctypes.c_int32), ("out", ctypes.c_void_p), ("ldo", ctypes.c_int64),
+                ("out_peers", ctypes.c_void_p * 7), ("n_peers", ctypes.c_int32)]
 
 
 APT_GROUP_MAX = 64
+APT_MAX_PEERS = 7
 APT_PACK_GROUP_MAX_ROWS = 64
 
 

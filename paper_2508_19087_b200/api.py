@@ -314,8 +314,10 @@ def gemm_grouped(problems, workspace: torch.Tensor | None = None, stream=None) -
 
     ``problems`` is a sequence of dicts with the keys of :func:`gemm`: ``W`` (tile-major Packed),
     ``A`` (Packed with its digit view), and optionally ``out_kind``, ``layout``, ``w_scale``,
-    ``a_scale``, ``w_zero``, ``a_zero``, ``w_gscale``, ``a_gscale``, ``out``.  Returns the list of
-    outputs; each equals ``gemm`` on the same arguments."""
+    ``a_scale``, ``w_zero``, ``a_zero``, ``w_gscale``, ``a_gscale``, ``out``, ``out_peers`` (up to 7
+    further outputs written with the same values at the same offsets: tensors shaped like ``out`` or device
+    pointers, e.g. symmetric-memory peer buffers, NEXT-4 ii).  Returns the list of outputs; each equals
+    ``gemm`` on the same arguments."""
     problems = list(problems)
     n = len(problems)
     if not 1 <= n <= L.APT_GROUP_MAX:
@@ -348,6 +350,14 @@ def gemm_grouped(problems, workspace: torch.Tensor | None = None, stream=None) -
         if sc is not None:
             p.scales = sc
         p.kind, p.layout, p.out, p.ldo = kind, lay, out.data_ptr(), out.stride(0)
+        peers = list(pr.get("out_peers") or [])
+        if len(peers) > L.APT_MAX_PEERS:
+            raise ValueError(f"problem {i}: at most {L.APT_MAX_PEERS} peer outputs")
+        for j, t in enumerate(peers):  # tensors shaped like out, or raw device pointers (symmetric memory)
+            if isinstance(t, torch.Tensor) and (t.dtype != dtype or tuple(t.shape) != shape or t.stride() != out.stride()):
+                raise ValueError(f"problem {i}: peer output {j} must match out's dtype, shape and strides")
+            p.out_peers[j] = t.data_ptr() if isinstance(t, torch.Tensor) else int(t)
+        p.n_peers = len(peers)
         outs.append(out)
     if workspace is None:
         workspace = grouped_workspace(dev)

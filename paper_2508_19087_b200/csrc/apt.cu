@@ -697,6 +697,12 @@ static apt_status grp_run(int32_t count, const apt_gemm_problem* problems, const
     e.kpad = (int32_t)kpad_of(K);
     e.h_w = 1 << (P.wbits - 1);
     e.h_a = 1 << (P.abits - 1);
+    if (P.n_peers < 0 || P.n_peers > APT_MAX_PEERS) return APT_ERR_INVALID_ARGUMENT;
+    q.n_peers = P.n_peers;
+    for (int j = 0; j < P.n_peers; ++j) {
+      if (!P.out_peers[j]) return APT_ERR_INVALID_ARGUMENT;
+      q.peers[j] = P.out_peers[j];
+    }
     q.w_zero = P.kind == APT_OUT_F16_SCALED ? P.scales.w_zero : nullptr;
     q.a_zero = P.kind == APT_OUT_F16_SCALED ? P.scales.a_zero : nullptr;
     q.w_gs = gs ? P.scales.w_gscale : nullptr;

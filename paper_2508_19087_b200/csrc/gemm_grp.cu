@@ -122,7 +122,14 @@ __device__ void grp_find(const GrpArgs& a, int w, int& p_out, int64_t& i_out, in
   g_out = a.total_blocks;
 }
 
-__device__ __forceinline__ void grp_store(const EpilogueArgs& e, int m, int n, uint32_t acc, int shift, int32_t ra,
+// one output element to out and to every peer buffer (NEXT-4 ii: epilogue-direct peer stores, same offset)
+template <typename T>
+__device__ __forceinline__ void grp_put(const GrpProblem& q, int64_t off, T v) {
+  reinterpret_cast<T*>(q.e.out)[off] = v;
+  for (int j = 0; j < q.n_peers; ++j) reinterpret_cast<T*>(q.peers[j])[off] = v;
+}
+
+__device__ __forceinline__ void grp_store(const GrpProblem& q, const EpilogueArgs& e, int m, int n, uint32_t acc, int shift, int32_t ra,
                                           int32_t rw, float wsc, float as, float az = 0.f, float wz = 0.f,
                                           bool zp = false) {
   // acc = U * 2^shift; Y = U - h_w RA - h_a RW - Kpad h_a h_w (mod 2^32, exact: reading Q8)
@@ -141,10 +148,10 @@ __device__ __forceinline__ void grp_store(const EpilogueArgs& e, int m, int n, u
     }
     unsigned short hv;
     asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hv) : "f"(v));
-    reinterpret_cast<unsigned short*>(e.out)[off] = hv;
+    grp_put<unsigned short>(q, off, hv);
   } else {
     const uint32_t yb = 4u * y + 2u * (uint32_t)ra + 2u * (uint32_t)rw + (uint32_t)e.K;  // Y' (I2)
-    reinterpret_cast<int32_t*>(e.out)[off] = (int32_t)(e.kind == 1 ? yb : y);
+    grp_put<int32_t>(q, off, (int32_t)(e.kind == 1 ? yb : y));
   }
 }
 
@@ -513,7 +520,6 @@ __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_
     if (epi && GS) {
       // group-wise scales: out = RN_fp16(sum_g ((float) Y_g * w_gscale) * a_gscale), fp16 row / column layout
       const EpilogueArgs& e = q.e;
-      unsigned short* out = reinterpret_cast<unsigned short*>(e.out);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int m = narrow ? 2 * t + (j & 1) : g + 8 * ((j >> 1) & 1);
@@ -521,7 +527,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_
         if ((narrow && j >= 8) || m >= e.M || n >= e.N) continue;
         unsigned short hv;
         asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hv) : "f"(__int_as_float(acc[j])));
-        out[e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m] = hv;
+        grp_put<unsigned short>(q, e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m, hv);
       }
     } else if (epi) {
       const EpilogueArgs& e = q.e;
@@ -547,7 +553,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_
             const float wz = (zp && q.w_zero) ? __ldg(q.w_zero + nc) : 0.f;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              grp_store(e, g + 8 * h, n, (uint32_t)acc[4 * qq + 2 * h + c], shift, ra[h], rw, wsc, as[h], az[h], wz, zp);
+              grp_store(q, e, g + 8 * h, n, (uint32_t)acc[4 * qq + 2 * h + c], shift, ra[h], rw, wsc, as[h], az[h], wz, zp);
           }
       } else {  // acc[4 P + 2 h + c]: weight row n_w + 16 P + g + 8 h, token 2t + c
         int32_t ra[2];
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_
             const float wz = (zp && q.w_zero) ? __ldg(q.w_zero + nc) : 0.f;
 #pragma unroll
             for (int c = 0; c < 2; ++c)
-              grp_store(e, 2 * t + c, n, (uint32_t)acc[4 * P + 2 * h + c], shift, ra[c], rw, wsc, as[c], az[c], wz, zp);
+              grp_store(q, e, 2 * t + c, n, (uint32_t)acc[4 * P + 2 * h + c], shift, ra[c], rw, wsc, as[c], az[c], wz, zp);
           }
       }
     }

@@ -129,6 +129,8 @@ struct GrpProblem {
   int64_t cost0;           // total cost of the blocks before the problem
   const float* w_zero;     // zero points [N] / [M] (fp16 output), nullable
   const float* a_zero;
+  void* peers[7];          // epilogue-direct peer stores: the output also goes to these (same offsets)
+  int32_t n_peers;
   const float* w_gs;       // group-wise (128) scales [Kpad / 128][N] (GS launches), else null
   const float* a_gs;       // [Kpad / 128][a_gs_ld], nullable (then a_scale per token)
   int64_t a_gs_ld;

@@ -102,3 +102,48 @@ def tp_gemm(W_local: api.Packed, A, n_total: int, out_kind: str = "i32",
     if comm is not None:
         torch.cuda.current_stream(device).wait_stream(comm)
     return out
+
+
+# ----------------------------------------------------------------------------- epilogue-direct peer stores
+
+def peer_slice_offset(rank: int, n_local: int, m: int, elem_bytes: int) -> int:
+    """Byte offset of rank `rank`'s slice (weight rows [rank n_local, (rank + 1) n_local)) in a gathered
+    column-layout output Y^T [world n_local, m]."""
+    return rank * n_local * m * elem_bytes
+
+
+def symmetric_outputs(shapes, dtype, group=None):
+    """Gathered outputs [N_total, M] in symmetric memory (torch.distributed._symmetric_memory) and their
+    rendezvous handles: every rank can store into every other rank's buffer over NVLink."""
+    import torch.distributed._symmetric_memory as symm_mem
+    dev = torch.device("cuda", torch.cuda.current_device())
+    grp = group if group is not None else dist.group.WORLD
+    bufs = [symm_mem.empty(tuple(sh), dtype=dtype, device=dev) for sh in shapes]
+    handles = [symm_mem.rendezvous(b, grp) for b in bufs]
+    return bufs, handles
+
+
+def tp_grouped_decode_peer(problems_local, gathered, handles, group=None, stream=None):
+    """N-split decode GEMMs whose epilogue is the all-gather (SURVEY §8f NEXT-4 ii).
+
+    ``problems_local`` are apt_gemm_grouped problems of this rank (``W`` = its row slice, tile-major; ``A``
+    replicated with its digit view; scales etc. as api.gemm_grouped); ``gathered[i]`` is the symmetric
+    [N_total, M] column-layout output of problem i and ``handles[i]`` its rendezvous handle.  Rank r writes
+    its slice Y_r^T into rows [r N/P, (r+1) N/P) of its own buffer AND of every peer's buffer straight from
+    the GEMM's epilogue (peer pointers of the symmetric allocation, same offsets), then one symmetric-memory
+    barrier makes every slice visible on every rank: no staging buffer, no collective copy."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    probs = []
+    for pr, buf, h in zip(problems_local, gathered, handles):
+        n_local, m = pr["W"].rows, pr["A"].rows
+        if buf.shape[0] != n_local * world or buf.shape[1] != m:
+            raise ValueError("gathered output must be [N_local * world, M]")
+        base = buf.data_ptr() - int(h.buffer_ptrs[rank])  # the tensor's offset inside the symmetric allocation
+        off = peer_slice_offset(rank, n_local, m, buf.element_size())
+        peers = [int(h.buffer_ptrs[j]) + base + off for j in range(world) if j != rank]
+        probs.append(dict(pr, layout="col", out=buf[rank * n_local:(rank + 1) * n_local], out_peers=peers))
+    api.gemm_grouped(probs, stream=stream)
+    if world > 1 and handles:
+        handles[0].barrier()  # stream-ordered: every rank's epilogue stores are visible after it
+    return gathered

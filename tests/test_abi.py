@@ -25,7 +25,7 @@ def test_header_symbols_exported():
     lib = L.lib()
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.apt_abi_version() == L.ABI_VERSION == 7
+    assert lib.apt_abi_version() == L.ABI_VERSION == 8
 
 
 def test_status_strings():

@@ -354,3 +354,59 @@ def test_zero_points_fused_decode(m):
     # the same problem inside a group with others
     outs = P.gemm_grouped([dict(W=W, A=A, **kw), _problem(16, 300, 700, 2, 2, seed=5, kind="f16")[0]])
     assert torch.equal(outs[0].view(torch.int16), fused.view(torch.int16))
+
+
+# ----------------------------------------------------------------------------- NEXT-4 ii: epilogue-direct peer stores
+
+@pytest.mark.parametrize("kind", ["i32", "f16", "gs"])
+def test_peer_outputs_bitwise(kind):
+    """The epilogue writes every element to out and to each peer output (up to 7) at the same offset:
+    every copy bit-identical to the plain output, in row and column layout."""
+    for layout in ("row", "col"):
+        prs = []
+        for i, (m, n, k, pw, pa) in enumerate([(16, 300, 1000, 4, 4), (1, 129, 513, 2, 2), (8, 256, 4096, 1, 8)]):
+            if kind == "gs":
+                pr, _ = _gs_problem(m, n, k, pw, pa, seed=80 + i, layout=layout)
+            else:
+                pr, _ = _problem(m, n, k, pw, pa, seed=80 + i, kind=kind, layout=layout)
+            prs.append(pr)
+        plain = [o.clone() for o in P.gemm_grouped(prs)]
+        peered = []
+        for pr, o in zip(prs, plain):
+            peers = [torch.full_like(o, 7) for _ in range(3 if kind == "i32" else 7)]
+            peered.append(peers)
+            pr["out_peers"] = peers
+            pr["out"] = torch.zeros_like(o)
+        outs = P.gemm_grouped(prs)
+        for o, p0, peers in zip(outs, plain, peered):
+            assert torch.equal(o.view(torch.int16) if o.dtype == torch.float16 else o,
+                               p0.view(torch.int16) if p0.dtype == torch.float16 else p0)
+            for t in peers:
+                assert torch.equal(t.view(torch.int16) if t.dtype == torch.float16 else t,
+                                   o.view(torch.int16) if o.dtype == torch.float16 else o)
+
+
+def test_tp_peer_decode_symmetric_memory_one_rank():
+    """tp.tp_grouped_decode_peer on a one-rank NCCL group with symmetric-memory outputs (the code path
+    of the multi-GPU decode; with one rank there are no peers, so this checks the plumbing and the slice
+    placement against the oracle).  Skipped when symmetric memory is unavailable."""
+    import os
+    import torch.distributed as dist
+    from paper_2508_19087_b200 import tp
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    try:
+        bufs, hs = tp.symmetric_outputs([(4096, 16), (11008, 8)], torch.float16)
+    except Exception as exc:  # pragma: no cover - depends on the driver / torch build
+        pytest.skip(f"symmetric memory unavailable: {exc!r}")
+    prs, refs = [], []
+    for i, (m, n, k, pw, pa) in enumerate([(16, 4096, 4096, 2, 2), (8, 11008, 4096, 4, 4)]):
+        pr, ref = _problem(m, n, k, pw, pa, seed=300 + i, kind="f16")
+        prs.append(pr)
+        refs.append(ref)
+    tp.tp_grouped_decode_peer(prs, bufs, hs)
+    torch.cuda.synchronize()
+    for b, (a, w, ws, as_, pw, pa) in zip(bufs, refs):
+        _check(b, "f16", "col", a, w, ws, as_, pw, pa, exact_ref=c_gemm_i64(a, w))

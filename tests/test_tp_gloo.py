@@ -79,3 +79,16 @@ def test_shard_rows():
     assert tp.shard_rows(8192, 4, 0) == (0, 2048)
     with pytest.raises(ValueError):
         tp.shard_rows(100, 8, 0)
+
+
+def test_peer_slice_offsets_tile_the_gathered_output():
+    """The byte offsets of the ranks' slices (epilogue-direct peer stores) tile the gathered column-layout
+    output exactly: rank r's rows [r n/P, (r+1) n/P) of Y^T [n, m], no overlap, no gap."""
+    from paper_2508_19087_b200 import tp
+    for world in (1, 2, 4, 8):
+        n, m, es = 4096, 16, 2
+        n_local = n // world
+        spans = [(tp.peer_slice_offset(r, n_local, m, es), tp.peer_slice_offset(r, n_local, m, es) + n_local * m * es)
+                 for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == n * m * es
+        assert all(spans[r][1] == spans[r + 1][0] for r in range(world - 1))

@@ -53,6 +53,13 @@ stream = torch.cuda.Stream()
 
 
 def time_variant(name, fn, reps=50):
+    try:
+        _time_variant(name, fn, reps)
+    except Exception as exc:  # e.g. a group larger than an experiment build's capacity
+        print(json.dumps({"variant": name, "error": repr(exc)[:200]}), flush=True)
+
+
+def _time_variant(name, fn, reps=50):
     with torch.cuda.stream(stream):
         fn(0)
         fn(1)
@@ -111,3 +118,30 @@ if len(sys.argv) > 1 and sys.argv[1] == "subsets":
         sub([i for i, c in enumerate(cases) if (c[3], c[4]) == (wb, ab)], f"grouped_W{wb}A{ab}")
     for m in MS:
         sub([i for i, c in enumerate(cases) if c[0] == m], f"grouped_M{m}")
+
+if len(sys.argv) > 1 and sys.argv[1] == "single":
+    def single_chain(s):
+        for pr in sets[s]:
+            P.gemm_grouped([pr], workspace=ws, stream=stream)
+    time_variant("grouped_single_problem_chain_36_launches", single_chain)
+    # per case: chained 36 launches of the same case (like tools/tune.py), grouped vs the selector's apt_gemm
+    for i, c in enumerate(cases):
+        pr0, pr1 = sets[0][i], sets[1][i]
+        ops1 = 2 * c[0] * c[1] * c[2]
+
+        def t_of(fn, n=40):
+            with torch.cuda.stream(stream):
+                for j in range(4):
+                    fn(j)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(stream)
+                for j in range(n):
+                    fn(j)
+                e1.record(stream)
+                torch.cuda.synchronize()
+            return e0.elapsed_time(e1) * 1e3 / n
+        tg = t_of(lambda j: P.gemm_grouped([pr0 if j % 2 else pr1], workspace=ws, stream=stream))
+        tc = t_of(lambda j: P.gemm((pr0 if j % 2 else pr1)["W"], pr0["A"], out_kind="f16", w_scale=pr0["w_scale"],
+                                    a_scale=pr0["a_scale"], out=pr0["out"], stream=stream))
+        print(json.dumps({"case": c, "grouped_us": round(tg, 2), "apt_gemm_us": round(tc, 2)}), flush=True)
