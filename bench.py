@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-baselines", action="store_true", help="skip cuBLAS / oracle / e2e legs")
     ap.add_argument("--decode", default="grouped", choices=["grouped", "per_call"],
                     help="decode GEMM phase: apt_gemm_grouped (one launch per precision) or 36 apt_gemm launches")
+    ap.add_argument("--tp-gather", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1, grouped decode: NCCL all-gather per output, or epilogue-direct peer stores into "
+                         "symmetric-memory outputs (tp.tp_grouped_decode_peer, NEXT-4 ii)")
     ap.add_argument("--legs", default="all",
                     help="extra BASELINE configs timed in the same run: all | none | comma list of prefill,llama70b,sweep")
     return ap.parse_args()
@@ -262,6 +265,10 @@ def main():
             for (m, wb, ab, n, k) in CASES]
     gathered = [torch.empty((n, m), dtype=torch.float16, device=dev) if world > 1 else None
                 for (m, wb, ab, n, k) in CASES]
+    peer = world > 1 and args.tp_gather == "peer" and args.decode == "grouped"
+    if peer:  # gathered outputs in symmetric memory: the grouped epilogue stores every rank's slice everywhere
+        from paper_2508_19087_b200 import tp
+        gathered, sym_h = tp.symmetric_outputs([(n, m) for (m, wb, ab, n, k) in CASES], torch.float16)
     cfgs = [P.select_config(m, shard[n], k, wb, ab) for (m, wb, ab, n, k) in CASES]
 
     # ---- offline weight packing (a1), timed once: outputs allocated first, one untimed pack per width
@@ -303,6 +310,12 @@ def main():
         is all-gathered."""
         if mode == "grouped":
             for idx in (PREC_IDX if groups is None else groups):
+                if peer and gather:  # NEXT-4 ii: the GEMM's epilogue is the all-gather
+                    tp.tp_grouped_decode_peer([dict(W=W_grp[wset][i], A=a_of(i), out_kind="f16",
+                                                    w_scale=W_scale[CASES[i][1:2] + CASES[i][3:]], a_scale=scale_of(i))
+                                               for i in idx], [gathered[i] for i in idx], [sym_h[i] for i in idx],
+                                              stream=stream)
+                    continue
                 P.gemm_grouped([dict(W=W_grp[wset][i], A=a_of(i), out_kind="f16", layout=layout,
                                      w_scale=W_scale[CASES[i][1:2] + CASES[i][3:]], a_scale=scale_of(i),
                                      out=out_of(i)) for i in idx], workspace=ws_grp, stream=stream)
@@ -451,7 +464,8 @@ def main():
                        "l2": ("inputs larger than L2: 2 alternating packed-weight sets (2 x 400 MB, every problem its "
                               "own weights)") if args.decode == "grouped" else
                              "inputs larger than L2: 2 alternating packed-weight sets (2 x 133 MB)",
-                       "parallelism": f"tp{world} (N-split + all-gather)" if world > 1 else "single GPU",
+                       "parallelism": (f"tp{world} (N-split + " + ("epilogue-direct peer stores" if peer else "NCCL all-gather")
+                                       + ")") if world > 1 else "single GPU",
                        "cuda_graphs": use_graphs},
             "gpu_launches": ((1 + len(PREC_IDX)) if grouped else (len(A_codes) + len(CASES))) * args.steps,
             "decode_path": ("apt_gemm_grouped: one persistent launch per precision (9 independent problems each, "

@@ -737,7 +737,9 @@ static apt_status grp_run(int32_t count, const apt_gemm_problem* problems, const
   ga.total_cost = cost;
   ga.tickets = reinterpret_cast<uint32_t*>(workspace);
   ga.partials = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(workspace) + APT_WS_TICKET_BYTES);
-  cudaError_t err = apt::launch_gemm_grp(ga, wbmax, (int)workers, gs, stream);
+  bool peers = false;
+  for (int i = 0; i < count; ++i) peers |= ga.p[i].n_peers > 0;
+  cudaError_t err = apt::launch_gemm_grp(ga, wbmax, (int)workers, gs, peers, stream);
   return err == cudaSuccess ? APT_OK : APT_ERR_CUDA;
 }
 

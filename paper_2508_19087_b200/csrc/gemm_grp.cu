@@ -122,13 +122,16 @@ __device__ void grp_find(const GrpArgs& a, int w, int& p_out, int64_t& i_out, in
   g_out = a.total_blocks;
 }
 
-// one output element to out and to every peer buffer (NEXT-4 ii: epilogue-direct peer stores, same offset)
-template <typename T>
+// one output element to out and, in launches with peers (a separate instantiation: even an untaken peer
+// branch cost the epilogue-light decode launches 6%), to every peer buffer at the same offset (NEXT-4 ii)
+template <bool PEERS, typename T>
 __device__ __forceinline__ void grp_put(const GrpProblem& q, int64_t off, T v) {
   reinterpret_cast<T*>(q.e.out)[off] = v;
-  for (int j = 0; j < q.n_peers; ++j) reinterpret_cast<T*>(q.peers[j])[off] = v;
+  if constexpr (PEERS)
+    for (int j = 0; j < q.n_peers; ++j) reinterpret_cast<T*>(q.peers[j])[off] = v;
 }
 
+template <bool PEERS>
 __device__ __forceinline__ void grp_store(const GrpProblem& q, const EpilogueArgs& e, int m, int n, uint32_t acc, int shift, int32_t ra,
                                           int32_t rw, float wsc, float as, float az = 0.f, float wz = 0.f,
                                           bool zp = false) {
@@ -148,10 +151,10 @@ __device__ __forceinline__ void grp_store(const GrpProblem& q, const EpilogueArg
     }
     unsigned short hv;
     asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hv) : "f"(v));
-    grp_put<unsigned short>(q, off, hv);
+    grp_put<PEERS, unsigned short>(q, off, hv);
   } else {
     const uint32_t yb = 4u * y + 2u * (uint32_t)ra + 2u * (uint32_t)rw + (uint32_t)e.K;  // Y' (I2)
-    grp_put<int32_t>(q, off, (int32_t)(e.kind == 1 ? yb : y));
+    grp_put<PEERS, int32_t>(q, off, (int32_t)(e.kind == 1 ? yb : y));
   }
 }
 
@@ -170,7 +173,7 @@ __device__ __forceinline__ void grp_wait(uint32_t bar, uint32_t parity) {
 #endif
 }
 
-template <int WBMAX, bool MT1, bool GS>
+template <int WBMAX, bool MT1, bool GS, bool PEERS>
 __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_constant__ GrpArgs a) {
   using SH = GrpShape<WBMAX>;
   constexpr int D = SH::kD;
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_
         if ((narrow && j >= 8) || m >= e.M || n >= e.N) continue;
         unsigned short hv;
         asm("cvt.rn.f16.f32 %0, %1;" : "=h"(hv) : "f"(__int_as_float(acc[j])));
-        grp_put<unsigned short>(q, e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m, hv);
+        grp_put<PEERS, unsigned short>(q, e.layout == 0 ? (int64_t)m * e.ldo + n : (int64_t)n * e.ldo + m, hv);
       }
     } else if (epi) {
       const EpilogueArgs& e = q.e;
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_
             const float wz = (zp && q.w_zero) ? __ldg(q.w_zero + nc) : 0.f;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              grp_store(q, e, g + 8 * h, n, (uint32_t)acc[4 * qq + 2 * h + c], shift, ra[h], rw, wsc, as[h], az[h], wz, zp);
+              grp_store<PEERS>(q, e, g + 8 * h, n, (uint32_t)acc[4 * qq + 2 * h + c], shift, ra[h], rw, wsc, as[h], az[h], wz, zp);
           }
       } else {  // acc[4 P + 2 h + c]: weight row n_w + 16 P + g + 8 h, token 2t + c
         int32_t ra[2];
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_
             const float wz = (zp && q.w_zero) ? __ldg(q.w_zero + nc) : 0.f;
 #pragma unroll
             for (int c = 0; c < 2; ++c)
-              grp_store(q, e, 2 * t + c, n, (uint32_t)acc[4 * P + 2 * h + c], shift, ra[c], rw, wsc, as[c], az[c], wz, zp);
+              grp_store<PEERS>(q, e, 2 * t + c, n, (uint32_t)acc[4 * P + 2 * h + c], shift, ra[c], rw, wsc, as[c], az[c], wz, zp);
           }
       }
     }
@@ -588,30 +591,37 @@ __global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_
   }
 }
 
-template <int WBMAX, bool MT1, bool GS>
+#ifndef APT_GRP_MT1
+#define APT_GRP_MT1 true
+#endif
+
+template <int WBMAX, bool MT1, bool GS, bool PEERS>
 static cudaError_t launch_grp2(const GrpArgs& a, int ctas, cudaStream_t stream) {
   constexpr int kSmem = GrpShape<WBMAX>::kSmem;
-  cudaError_t err = set_smem_once<gemm_grp_kernel<WBMAX, MT1, GS>>(kSmem);
+  cudaError_t err = set_smem_once<gemm_grp_kernel<WBMAX, MT1, GS, PEERS>>(kSmem);
   if (err != cudaSuccess) return err;
-  return launch_pdl(gemm_grp_kernel<WBMAX, MT1, GS>, dim3(ctas), dim3(160), kSmem, stream, dim3(1, 1, 1), a);
+  return launch_pdl(gemm_grp_kernel<WBMAX, MT1, GS, PEERS>, dim3(ctas), dim3(160), kSmem, stream, dim3(1, 1, 1), a);
+}
+
+template <bool PEERS>
+static cudaError_t launch_grp1(const GrpArgs& a, int cls, bool gs, int ctas, cudaStream_t stream) {
+  switch (cls * 2 + (gs ? 1 : 0)) {
+    case 4: return launch_grp2<2, APT_GRP_MT1, false, PEERS>(a, ctas, stream);
+    case 5: return launch_grp2<2, APT_GRP_MT1, true, PEERS>(a, ctas, stream);
+    case 8: return launch_grp2<4, APT_GRP_MT1, false, PEERS>(a, ctas, stream);
+    case 9: return launch_grp2<4, APT_GRP_MT1, true, PEERS>(a, ctas, stream);
+    case 17: return launch_grp2<8, APT_GRP_MT1, true, PEERS>(a, ctas, stream);
+    default: return launch_grp2<8, APT_GRP_MT1, false, PEERS>(a, ctas, stream);
+  }
 }
 
 int grp_wbmax_class(int wbmax) { return wbmax <= 2 ? 2 : wbmax <= 4 ? 4 : 8; }
 // CTAs per SM (shared memory: 3 x 72 KB at WBMAX 2, 3 x 60 KB at WBMAX 4, 2 x 108 KB at WBMAX 8)
 int grp_ctas_per_sm(int wbmax, bool gs) { return gs ? 2 : grp_wbmax_class(wbmax) <= 4 ? 3 : 2; }
 
-#ifndef APT_GRP_MT1
-#define APT_GRP_MT1 true
-#endif
-cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, cudaStream_t stream) {
-  switch (grp_wbmax_class(wbmax) * 2 + (gs ? 1 : 0)) {
-    case 4: return launch_grp2<2, APT_GRP_MT1, false>(a, ctas, stream);
-    case 5: return launch_grp2<2, APT_GRP_MT1, true>(a, ctas, stream);
-    case 8: return launch_grp2<4, APT_GRP_MT1, false>(a, ctas, stream);
-    case 9: return launch_grp2<4, APT_GRP_MT1, true>(a, ctas, stream);
-    case 17: return launch_grp2<8, APT_GRP_MT1, true>(a, ctas, stream);
-    default: return launch_grp2<8, APT_GRP_MT1, false>(a, ctas, stream);
-  }
+cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, bool peers, cudaStream_t stream) {
+  const int cls = grp_wbmax_class(wbmax);
+  return peers ? launch_grp1<true>(a, cls, gs, ctas, stream) : launch_grp1<false>(a, cls, gs, ctas, stream);
 }
 
 }  // namespace apt

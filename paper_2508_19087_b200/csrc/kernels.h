@@ -145,5 +145,5 @@ struct GrpArgs {
 };
 int grp_wbmax_class(int wbmax);
 int grp_ctas_per_sm(int wbmax, bool gs);
-cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, cudaStream_t stream);
+cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, bool peers, cudaStream_t stream);
 }  // namespace apt

@@ -1,7 +1,5 @@
-# GPU session script (edited per call)
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "pack or digit or quant or repack or smoke" 2>&1 | tail -3 > gpurun_out/r2_pack_test.txt
-timeout 600 python tools/pack_bench.py > gpurun_out/r2_pack_bench2.jsonl 2>&1
-timeout 900 python bench.py --steps 50 --warmup 5 --no-baselines --legs none > gpurun_out/r2_bench8.json 2> gpurun_out/r2_bench8.err
-cat gpurun_out/r2_pack_test.txt
+timeout 900 python -m pytest tests/test_gpu_grouped.py -x -q 2>&1 | tail -3 > gpurun_out/grp_test.txt
+timeout 600 python tools/grp_bench.py 2>&1 | grep "per_precision\|1_launch" >> gpurun_out/grp_test.txt
+cat gpurun_out/grp_test.txt
