@@ -624,7 +624,7 @@ int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, in
 }
 
 // ---- grouped decode GEMM (include/apt.h apt_gemm_grouped, gemm_grp.cu)
-static int grp_max_workers() { return device_sms() * 3; }  // one worker per CTA, at most 3 CTAs per SM
+static int grp_max_workers() { return device_sms() * 4; }  // one worker per CTA, at most 4 CTAs per SM
 
 size_t apt_gemm_grouped_workspace_bytes(int32_t count) {
   if (count < 1 || count > APT_GROUP_MAX) return 0;

@@ -44,7 +44,7 @@ struct GrpShape {
 #ifdef APT_GRP_D
   static constexpr int kD = APT_GRP_D;
 #else
-  static constexpr int kD = WBMAX <= 2 ? 6 : WBMAX <= 4 ? 3 : 3;
+  static constexpr int kD = WBMAX <= 2 ? 4 : 2;  // 48 / 40 / 72 KB per CTA: 4 / 4 / 3 CTAs per SM
 #endif
   static constexpr int kBarOff = kD * kSlot;
   static constexpr int kSmem = kBarOff + 2 * kD * 8 + 16;
@@ -173,8 +173,11 @@ __device__ __forceinline__ void grp_wait(uint32_t bar, uint32_t parity) {
 #endif
 }
 
+#ifndef APT_GRP_MINB
+#define APT_GRP_MINB 4  // four CTAs per SM (<= 102 registers): more consumer warps beat deeper rings (measured)
+#endif
 template <int WBMAX, bool MT1, bool GS, bool PEERS>
-__global__ void __launch_bounds__(160, GS ? 2 : 3) gemm_grp_kernel(const __grid_constant__ GrpArgs a) {
+__global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(const __grid_constant__ GrpArgs a) {
   using SH = GrpShape<WBMAX>;
   constexpr int D = SH::kD;
   extern __shared__ __align__(1024) uint8_t smem[];  // no static shared memory: the swizzled token
@@ -616,8 +619,9 @@ static cudaError_t launch_grp1(const GrpArgs& a, int cls, bool gs, int ctas, cud
 }
 
 int grp_wbmax_class(int wbmax) { return wbmax <= 2 ? 2 : wbmax <= 4 ? 4 : 8; }
-// CTAs per SM (shared memory: 3 x 72 KB at WBMAX 2, 3 x 60 KB at WBMAX 4, 2 x 108 KB at WBMAX 8)
-int grp_ctas_per_sm(int wbmax, bool gs) { return gs ? 2 : grp_wbmax_class(wbmax) <= 4 ? 3 : 2; }
+// CTAs per SM (shared memory 48 / 40 / 72 KB per CTA at WBMAX 2 / 4 / 8; registers: <= 102 per thread
+// for four CTAs; the group-scale path needs more registers: two)
+int grp_ctas_per_sm(int wbmax, bool gs) { return gs ? 2 : grp_wbmax_class(wbmax) <= 4 ? 4 : 3; }
 
 cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, bool peers, cudaStream_t stream) {
   const int cls = grp_wbmax_class(wbmax);

@@ -197,4 +197,4 @@ def test_grouped_argument_errors_without_gpu():
     arr[0].M = 17  # more tokens than the decode kernel's 16
     assert lib.apt_gemm_grouped(1, arr, None, 0, None) == L.APT_ERR_INVALID_ARGUMENT
     assert lib.apt_gemm_grouped_workspace_bytes(0) == 0
-    assert lib.apt_gemm_grouped_workspace_bytes(1) >= 16384 + 148 * 3 * 2 * 4 * 512 * 4
+    assert lib.apt_gemm_grouped_workspace_bytes(1) >= 16384 + 148 * 4 * 2 * 4 * 512 * 4
