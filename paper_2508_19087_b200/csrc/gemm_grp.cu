@@ -440,7 +440,9 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
         // this warp is done with the slot: order its generic-proxy reads before the producer's next
         // async-proxy (bulk copy / TMA) write of the slot, then release it.  The fence sits here, not in
         // the producer: there it would also wait for the producer's own bulk copies in flight.
+#ifndef APT_GRP_NOFENCE
         fence_proxy_async();
+#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(empty(slot));
         if (++slot == D) {
