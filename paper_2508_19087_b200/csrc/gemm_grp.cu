@@ -5,25 +5,28 @@
 // Why: a single decode GEMM streams 2-23 MB of packed weights, i.e. 0.3-3.5 us at HBM speed, while a
 // launch costs ~1 us of prologue and another ~1 us before its first weight bytes arrive
 // (profiles/r2_dec_trace.txt, r2_chain_floor.json); chained, the per-GEMM kernels spend as much time
-// ramping up and draining as streaming.  Here every warp is an independent worker that streams its
-// share of ALL the problems' weights through one continuous shared-memory ring, so HBM never sees a
-// launch boundary inside the group.
+// ramping up and draining as streaming.  Here the CTAs of one grid split the SUM of all problems'
+// weight blocks, so HBM never sees a launch boundary inside the group.
 //
-// Work decomposition (stream-K over the group): the unit is a block = 32 weight rows x 256 K elements
-// of one problem (problem-major, then row tile, then K).  Blocks carry a cost (2 p_w + 1: the packed
-// bytes plus a fixed share for the token fragments and MMAs) and every warp takes one contiguous
-// range of equal total cost (midpoint rule, integer arithmetic, so every warp computes every other
-// warp's range without communication).  A warp accumulates consecutive blocks of the same row tile in
-// registers; a tile covered by one warp goes straight to the epilogue, a tile split between warps
-// writes int32 partials ([worker][2][16 x 32]) and the last warp to take the tile's ticket (acq_rel,
-// keyed by the tile's first worker) adds them and runs the epilogue.
+// Work decomposition (stream-K over the group): the unit is 128 weight rows x 256 K elements of one
+// problem (problem-major, then 128-row tile, then K).  Units carry a cost (4 p_w + 2: the packed KB
+// plus a fixed share for tokens and MMAs) and every CTA takes one contiguous range of equal total cost
+// (midpoint rule, integer arithmetic: every CTA computes every other CTA's range without communication).
+// A CTA accumulates consecutive units of a tile in registers; a tile covered by one CTA goes straight to
+// the epilogue, a tile split between CTAs is reduced per 32-row warp slice: int32 partials
+// ([worker][2][4 warps][16 x 32]) and an acq_rel ticket per slice, the last arrival adds and stores.
 //
-// Per block a lane (g, t) = (lane / 4, lane % 4) computes exactly what gemm_dec.cu computes (same
-// digit rebuild — rebuild_hi / rebuild_x16 / rebuild8, the shift half of the shift-add recovery,
-// P:228 —, the same mma.sync.m16n8k32 u8 fragments with the weights as the B operand and the tokens
-// g, g + 8 of the activation digit view as the A operand, the same rank-1 correction and epilogue);
-// only the weight staging differs: 16-byte cp.async copies of whole 512-byte runs of the tile-major
-// layout, lane = weight row, read back by the MMA lanes after a warp barrier.
+// CTA = 1 producer warp + 4 consumer warps.  The producer lane moves each unit into a ring slot with
+// one cp.async.bulk per weight plane (4 KB: a 128-row x 256-K block of the tile-major layout is
+// contiguous) and two 2-D TMA boxes of the activation digit view (M rows x 128 bytes, 128-byte swizzle),
+// completing on the slot's full mbarrier.  Consumer warp cw owns rows 32 cw .. 32 cw + 31 of the tile;
+// lane (g, t) = (lane / 4, lane % 4) takes words t and t + 4 of the block for BOTH operands (so K
+// agrees; conflict-free shared-memory reads), rebuilds the weight digits (rebuild_hi / rebuild_x16 /
+// rebuild8: the shift half of the shift-add recovery) and issues mma.sync.m16n8k32 u8 with the
+// weights as the B operand and tokens g, g + 8 as A (M > 8), or the weights as A (16 rows per MMA) and
+// tokens g as B (M <= 8, half the MMAs); the epilogue is gemm_dec.cu's (rank-1 correction, scales,
+// zero points, fp16 / int32, row / column layout; optionally also stored to peer buffers).  Group-wise
+// scales use signed digits and s8 MMAs so that every 128-element group's product is exact on its own.
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>
