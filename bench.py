@@ -5,8 +5,8 @@ Default workload (BASELINE.json configs[1], "llama2-7b-decode"): one STEP is the
 hot path for every Llama-2-7B decode linear (N x K = 4096x4096, 11008x4096, 4096x11008) at
 M = 1, 8, 16 tokens and W1A2, W2A2, W3A4, W4A4 (36 cases): the 12 distinct activations packed
 (apt_pack_bipolar), then the 36 bit-plane GEMMs with the fused fp16 scale epilogue.  The 36 GEMMs are
-independent problems; by default (--decode grouped) they run through apt_gemm_grouped, one persistent
-launch per precision (9 problems each), every problem with its OWN packed weights (3 copies per linear,
+independent problems; by default (--decode grouped) they run through apt_gemm_grouped, ONE persistent
+launch for all 36 problems (the 12 activation packs: one apt_pack_grouped launch), every problem with its OWN packed weights (3 copies per linear,
 so no problem reads another's weights from L2); --decode per_call runs 36 apt_gemm launches instead (the
 per-GEMM path, also reported under `per_call` in the default run).  Weight packing is offline (done once,
 timed separately and reported as `weight_pack`).  Two packed-weight sets (2 x 400 MB grouped, 2 x 133 MB
@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--impl", default="apt", choices=["apt", "reference"])
     ap.add_argument("--no-baselines", action="store_true", help="skip cuBLAS / oracle / e2e legs")
     ap.add_argument("--decode", default="grouped", choices=["grouped", "per_call"],
-                    help="decode GEMM phase: apt_gemm_grouped (one launch per precision) or 36 apt_gemm launches")
+                    help="decode GEMM phase: apt_gemm_grouped (one launch of the 36 problems) or 36 apt_gemm launches")
     ap.add_argument("--tp-gather", default="nccl", choices=["nccl", "peer"],
                     help="N > 1, grouped decode: NCCL all-gather per output, or epilogue-direct peer stores into "
                          "symmetric-memory outputs (tp.tp_grouped_decode_peer, NEXT-4 ii)")
@@ -291,6 +291,9 @@ def main():
     # share a weight buffer, so no problem's weights are served from L2 by another's reads), 2 sets
     W_grp = [[P.pack(codes(shard[n], k, wb), wb, tiled=True) for (m, wb, ab, n, k) in CASES] for _ in range(2)]
     PREC_IDX = [[i for i, c in enumerate(CASES) if (c[1], c[2]) == pq] for pq in PRECISIONS]
+    # the step's grouped launches: all 36 problems in ONE launch (stream-K balances the mixed widths and
+    # token counts; measured faster than one launch per precision, which `per_precision` times)
+    STEP_GROUPS = [list(range(len(CASES)))]
     ws_grp = P.grouped_workspace(dev)
 
     # one step = pack every distinct activation (m, abits, K) once (12 packs; the 4096x4096 and 11008x4096
@@ -309,7 +312,7 @@ def main():
         which problems share a launch) or one apt_gemm per case (mode "per_call"); at N > 1 each output slice
         is all-gathered."""
         if mode == "grouped":
-            for idx in (PREC_IDX if groups is None else groups):
+            for idx in (STEP_GROUPS if groups is None else groups):
                 if peer and gather:  # NEXT-4 ii: the GEMM's epilogue is the all-gather
                     tp.tp_grouped_decode_peer([dict(W=W_grp[wset][i], A=a_of(i), out_kind="f16",
                                                     w_scale=W_scale[CASES[i][1:2] + CASES[i][3:]], a_scale=scale_of(i))
@@ -467,11 +470,11 @@ def main():
                        "parallelism": (f"tp{world} (N-split + " + ("epilogue-direct peer stores" if peer else "NCCL all-gather")
                                        + ")") if world > 1 else "single GPU",
                        "cuda_graphs": use_graphs},
-            "gpu_launches": ((1 + len(PREC_IDX)) if grouped else (len(A_codes) + len(CASES))) * args.steps,
-            "decode_path": ("apt_gemm_grouped: one persistent launch per precision (9 independent problems each, "
-                            "every problem its own packed weights)") if grouped else "36 apt_gemm launches",
+            "gpu_launches": ((1 + len(STEP_GROUPS)) if grouped else (len(A_codes) + len(CASES))) * args.steps,
+            "decode_path": ("apt_gemm_grouped: one persistent launch of the 36 independent problems (every problem "
+                            "its own packed weights)") if grouped else "36 apt_gemm launches",
             "roofline": {"bound": "hbm",
-                         "kernel": ("gemm_grp_kernel (apt_gemm_grouped) x4 launches/step" if grouped else
+                         "kernel": ("gemm_grp_kernel (apt_gemm_grouped) x1 launch/step" if grouped else
                                     "decode GEMM phase: " + ", ".join(
                                         f"{k} x{v}" for k, v in sorted(kernel_mix(cfgs).items())) + " launches/step"),
                          "measured": "GEMM phase replayed alone right after the timed region (events around the graph "
@@ -481,9 +484,9 @@ def main():
                          "frac": round(achieved / hbm_peak, 4),
                          "traffic": traffic.get("dram_bytes_per_launch_avg") if traffic else None,
                          "traffic_source": (traffic or {}).get("source"),
-                         "alg_bytes_per_launch_avg": round(bytes_all / (len(PREC_IDX) if grouped else len(CASES))),
+                         "alg_bytes_per_launch_avg": round(bytes_all / (len(STEP_GROUPS) if grouped else len(CASES))),
                          "gemm_share_of_step": round(gemm_ms / ms_per_step, 3),
-                         "gemm_us_per_launch": round(1e3 * gemm_ms / (len(PREC_IDX) if grouped else len(CASES)), 3)},
+                         "gemm_us_per_launch": round(1e3 * gemm_ms / (len(STEP_GROUPS) if grouped else len(CASES)), 3)},
             "act_pack": {"launches_per_step": 1 if grouped else len(A_codes), "packs_per_step": len(A_codes),
                          "us_per_step": round(1e3 * pack_ms, 3),
                          "path": "apt_pack_grouped (12 packs, one launch)" if grouped else "12 apt_pack_bipolar"},
@@ -868,7 +871,7 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
         s1.record()
         barrier()
         e2e_ms = s0.elapsed_time(s1) / n_e2e
-        gm = "4x apt_gemm_grouped (36 GEMMs, fp16)" if args.decode == "grouped" else "36x apt_gemm (fp16)"
+        gm = "1x apt_gemm_grouped (36 GEMMs, fp16)" if args.decode == "grouped" else "36x apt_gemm (fp16)"
         qp = "apt_pack_grouped (12 quantize + packs)" if args.decode == "grouped" else "12x apt_quantize_pack"
         pp = "apt_pack_grouped (12 packs)" if args.decode == "grouped" else "12x apt_pack_bipolar"
         path = (f"pinned host fp16 activations -> 1 H2D -> {qp} -> {gm} -> 1 D2H"
@@ -955,7 +958,7 @@ def baselines(args, P, dev, stream, world, rank, shard, W_packed, W_scale, A_sca
         torch.cuda.synchronize()
         barrier()
         e2e_ms = s0.elapsed_time(s1) / n_e2e
-        gm = "4x apt_gemm_grouped (36 GEMMs, fp16)" if args.decode == "grouped" else "36x apt_gemm (fp16)"
+        gm = "1x apt_gemm_grouped (36 GEMMs, fp16)" if args.decode == "grouped" else "36x apt_gemm (fp16)"
         qp = "apt_pack_grouped (12 quantize + packs)" if args.decode == "grouped" else "12x apt_quantize_pack"
         pp = "apt_pack_grouped (12 packs)" if args.decode == "grouped" else "12x apt_pack_bipolar"
         path = (f"pinned host fp16 activations -> H2D -> {qp} -> {gm} -> D2H" if fp16

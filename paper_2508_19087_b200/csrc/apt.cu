@@ -712,7 +712,9 @@ static apt_status grp_run(int32_t count, const apt_gemm_problem* problems, const
     q.nb = P.W.k_words / 8;  // units of 128 rows x 256 K per 128-row tile
     q.tiles = (N + 127) / 128;
     q.wbits = P.wbits;
-    q.cost = 4 * P.wbits + 2;  // KB of packed weights per unit + a fixed share (tokens, MMAs)
+    // KB of packed weights per unit + a share for the token tile and the MMAs: M > 8 takes the two-token-
+    // tile MMA orientation (twice the MMAs and token bytes; measured ~1.4x the unit time of M <= 8)
+    q.cost = 4 * P.wbits + (M > 8 ? 8 : 2);
     q.blk0 = blocks;
     q.cost0 = cost;
     blocks += (int64_t)q.tiles * q.nb;
