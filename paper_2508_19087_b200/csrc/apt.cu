@@ -712,9 +712,16 @@ static apt_status grp_run(int32_t count, const apt_gemm_problem* problems, const
     q.nb = P.W.k_words / 8;  // units of 128 rows x 256 K per 128-row tile
     q.tiles = (N + 127) / 128;
     q.wbits = P.wbits;
-    // KB of packed weights per unit + a share for the token tile and the MMAs: M > 8 takes the two-token-
-    // tile MMA orientation (twice the MMAs and token bytes; measured ~1.4x the unit time of M <= 8)
-    q.cost = 4 * P.wbits + (M > 8 ? 8 : 2);
+    // unit cost = 4 KB per weight plane + a fixed share for the consumers' per-unit work (token tile,
+    // MMAs, barriers), twice as large at M > 8 (the two-token-tile orientation: twice the MMAs and token
+    // bytes).  Coefficients fitted on the bench's 36-problem launch (tools/grp_bench.py): 4 / 2 per plane
+    // + 16 / 8 ran it in 120 us, 4 + 2 (bytes only) in 150 us, 4 + 8 / 2 in 132 us
+#ifndef APT_GRP_CW
+#define APT_GRP_CW 4
+#define APT_GRP_CM16 16
+#define APT_GRP_CM8 8
+#endif
+    q.cost = APT_GRP_CW * P.wbits + (M > 8 ? APT_GRP_CM16 : APT_GRP_CM8);
     q.blk0 = blocks;
     q.cost0 = cost;
     blocks += (int64_t)q.tiles * q.nb;
