@@ -1,0 +1,61 @@
+"""Per-unit timeline of one grouped launch (APT_LIB_VARIANT=libapt_trace.so, built with -DAPT_GRP_TRACE):
+data latency (weights issued -> consumer warp 0 sees the slot full), consumer time (full -> released),
+producer wait (released u - D -> weights of u issued).  usage: python tools/grp_trace.py W1A2|W4A4"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2508_19087_b200 as P  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "W1A2"
+wb, ab = {"W1A2": (1, 2), "W2A2": (2, 2), "W3A4": (3, 4), "W4A4": (4, 4)}[which]
+dev = torch.device("cuda:0")
+probs = []
+for (n, k) in [(4096, 4096), (11008, 4096), (4096, 11008)]:
+    for m in (1, 8, 16):
+        w = torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev)
+        a = torch.randint(-(1 << (ab - 1)), 1 << (ab - 1), (m, k), dtype=torch.int8, device=dev)
+        probs.append(dict(W=P.pack(w, wb, tiled=True), A=P.pack(a, ab, digits=True), out_kind="f16",
+                          w_scale=torch.rand(n, device=dev), a_scale=torch.rand(m, device=dev)))
+ws = P.grouped_workspace(dev)
+L = P._lib.lib()
+fn = L.apt_debug_grp_trace
+fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+for _ in range(3):
+    P.gemm_grouped(probs, workspace=ws)
+torch.cuda.synchronize()
+fn(None, 1)
+torch.cuda.synchronize()
+P.gemm_grouped(probs, workspace=ws)
+torch.cuda.synchronize()
+buf = np.zeros((1024, 48, 4), dtype=np.uint64)
+fn(buf.ctypes.data, 0)
+t = buf.astype(np.float64)
+ctas = np.nonzero(t[:, 0, 0])[0]
+t0 = t[ctas][:, :, :][t[ctas] > 0].min()
+lat, comp, pw, gap = [], [], [], []
+D = 4 if wb <= 2 else 2
+for c in ctas:
+    u_n = int(np.count_nonzero(t[c, :, 3]))
+    for u in range(u_n):
+        if t[c, u, 0] and t[c, u, 2]:
+            lat.append(t[c, u, 2] - t[c, u, 0])
+        if t[c, u, 2] and t[c, u, 3]:
+            comp.append(t[c, u, 3] - t[c, u, 2])
+        if u >= D and t[c, u, 0] and t[c, u - D, 3]:
+            pw.append(t[c, u, 0] - t[c, u - D, 3])
+        if u >= 1 and t[c, u, 2] and t[c, u - 1, 3]:
+            gap.append(t[c, u, 2] - t[c, u - 1, 3])
+q = lambda v: (round(float(np.percentile(v, 10)), 0), round(float(np.median(v)), 0), round(float(np.percentile(v, 90)), 0))  # noqa: E731
+print(which, "ctas", len(ctas), "units/cta med", int(np.median([np.count_nonzero(t[c, :, 3]) for c in ctas])))
+print("span us", round((t[ctas].max() - t0) / 1e3, 2), "first issue -> first full med ns", q([t[c, 0, 2] - t[c, 0, 0] for c in ctas]))
+print("data latency issue->full ns (p10, med, p90)", q(lat))
+print("consumer full->release ns", q(comp))
+print("consumer idle release(u-1)->full(u) ns", q(gap))
+print("producer release(u-D)->issue(u) ns", q(pw))
+print("cta start (first issue) spread us", round((t[ctas, 0, 0].max() - t[ctas, 0, 0].min()) / 1e3, 2),
+      "cta end spread us", round((max(t[c, :, 3].max() for c in ctas) - min(t[c, :, 3].max() for c in ctas)) / 1e3, 2))
