@@ -62,6 +62,20 @@ __device__ __forceinline__ void grp_rebuild(const uint32_t* w, uint32_t (&o)[8])
 // digits are u * 2^shift (gemm_dec.cu DecShape::kShift)
 __device__ __forceinline__ int grp_shift(int wb) { return wb <= 2 ? 8 - wb : wb <= 4 ? 4 : 0; }
 
+#ifdef APT_GRP_TRACE
+// per-unit globaltimer timeline (profiling builds only): [cta][unit < 48][0 weights issued, 1 tokens
+// issued, 2 consumer warp 0 saw full, 3 consumer warp 0 released]
+__device__ unsigned long long g_grp_trace[1024][48][4];
+__device__ __forceinline__ unsigned long long grp_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define GRP_TRACE(u, ph) do { if ((u) < 48 && blockIdx.x < 1024) g_grp_trace[blockIdx.x][(u)][(ph)] = grp_gtimer(); } while (0)
+#else
+#define GRP_TRACE(u, ph) do { } while (0)
+#endif
+
 __device__ __forceinline__ void grp_mma(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                         uint32_t b1) {
   asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
@@ -258,6 +272,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
       const int qp = pp, qt = ptile, qb = pblk;
       for (int u = 0; u < pre; ++u) {
         weights(u);
+        GRP_TRACE(u, 0);
         advance();
       }
       pdl_wait();
@@ -267,6 +282,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
       load_problem();
       for (int u = 0; u < pre; ++u) {
         tokens(u);
+        GRP_TRACE(u, 1);
         advance();
       }
     }
@@ -275,7 +291,9 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
     for (int64_t u = pre; u < U; ++u) {
       grp_wait(empty(slot), (ph & 1) ^ 1);  // (the consumers fence their generic reads of the slot)
       weights(slot);
+      GRP_TRACE(u, 0);
       tokens(slot);
+      GRP_TRACE(u, 1);
       advance();
       if (++slot == D) {
         slot = 0;
@@ -293,6 +311,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
   int64_t ci = i0, cg = gstart;
   int slot = 0;
   uint32_t ph = 0;
+  [[maybe_unused]] int tu = 0;  // units consumed (trace index)
 #pragma unroll 1
   while (cg < gend) {
     const GrpProblem& q = a.p[cp];
@@ -346,6 +365,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
           }
         }
         grp_wait(full(slot), ph & 1);
+        if (cw == 0 && lane == 0) GRP_TRACE(tu, 2);
         const uint32_t sl = sbase + (uint32_t)(slot * SH::kSlot);
         uint4 tk0[4], tk1[4];  // [2 box + k]: word t (box 0) then word t + 4 (box 1), rows g / g + 8
 #pragma unroll
@@ -448,6 +468,8 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
 #endif
         __syncwarp();
         if (lane == 0) mbar_arrive(empty(slot));
+        if (cw == 0 && lane == 0) GRP_TRACE(tu, 3);
+        ++tu;
         if (++slot == D) {
           slot = 0;
           ++ph;
@@ -634,3 +656,13 @@ cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, bool
 }
 
 }  // namespace apt
+
+#ifdef APT_GRP_TRACE
+extern "C" __attribute__((visibility("default"))) int apt_debug_grp_trace(unsigned long long* host, int reset) {
+  if (reset) {
+    static unsigned long long zero[1024 * 48 * 4];
+    return (int)cudaMemcpyToSymbol(apt::g_grp_trace, zero, sizeof(zero));
+  }
+  return (int)cudaMemcpyFromSymbol(host, apt::g_grp_trace, sizeof(unsigned long long) * 1024 * 48 * 4);
+}
+#endif
