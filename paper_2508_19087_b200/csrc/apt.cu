@@ -744,6 +744,11 @@ static apt_status grp_run(int32_t count, const apt_gemm_problem* problems, const
   ga.workers = (int32_t)workers;
   ga.total_blocks = blocks;
   ga.total_cost = cost;
+  for (int i = 0; i < count; ++i) {  // owner of each problem's last block (gemm_grp.cu grp_owner, same formula)
+    const apt::GrpProblem& q = ga.p[i];
+    const int64_t last = (int64_t)q.tiles * q.nb - 1;
+    ga.p[i].w_hi = (int32_t)((2 * q.cost0 + (2 * last + 1) * (int64_t)q.cost) * workers / (2 * cost));
+  }
   ga.tickets = reinterpret_cast<uint32_t*>(workspace);
   ga.partials = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(workspace) + APT_WS_TICKET_BYTES);
   bool peers = false;

@@ -121,7 +121,7 @@ __device__ void grp_find(const GrpArgs& a, int w, int& p_out, int64_t& i_out, in
   for (int p = 0; p < a.count; ++p) {
     const GrpProblem& q = a.p[p];
     const int64_t nblk = (int64_t)q.tiles * q.nb;
-    if (grp_owner(a, q, nblk - 1) < w) continue;
+    if (q.w_hi < w) continue;  // == grp_owner(a, q, nblk - 1), precomputed on the host
     // owner(i) >= w  <=>  (2 cost0 + (2 i + 1) c) W >= 2 w T
     const int64_t cW = (int64_t)q.cost * a.workers;
     const int64_t num = 2 * (int64_t)w * a.total_cost - 2 * q.cost0 * a.workers;
@@ -538,9 +538,16 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
       epi = prev == (unsigned)(lw - fw);
       if (epi) {
         __syncwarp();
+        // int32 partials add exactly in any order; the fp32 group-scale sums are added in worker order
+        // (this warp's own slice re-read from memory in its place), so the rounding does not depend on
+        // which CTA happened to arrive last
+        if constexpr (GS) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = __float_as_int(0.f);
+        }
 #pragma unroll 1
         for (int o = fw; o <= lw; ++o) {
-          if (o == w) continue;
+          if (!GS && o == w) continue;
           const int* po = a.partials + (((int64_t)o * 2 + (o == fw ? 1 : 0)) * 4 + cw) * 512;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {

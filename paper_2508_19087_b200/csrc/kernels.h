@@ -127,6 +127,8 @@ struct GrpProblem {
   EpilogueArgs e;
   int64_t blk0;            // global index of the problem's first block (tile-major, then K)
   int64_t cost0;           // total cost of the blocks before the problem
+  int32_t w_hi;            // worker owning the problem's last block (host-computed: grp_find skips whole
+                           // problems with one compare instead of a 64-bit division each)
   const float* w_zero;     // zero points [N] / [M] (fp16 output), nullable
   const float* a_zero;
   void* peers[7];          // epilogue-direct peer stores: the output also goes to these (same offsets)

@@ -410,3 +410,16 @@ def test_tp_peer_decode_symmetric_memory_one_rank():
     torch.cuda.synchronize()
     for b, (a, w, ws, as_, pw, pa) in zip(bufs, refs):
         _check(b, "f16", "col", a, w, ws, as_, pw, pa, exact_ref=c_gemm_i64(a, w))
+
+
+def test_group_scales_deterministic():
+    """The fp32 group-scale sums of a row tile split between CTAs are added in a fixed order: repeated
+    launches give identical bits (the 9 decode shapes of W4A4, many split tiles)."""
+    prs = []
+    for (n, k) in LLAMA7B:
+        for m in (1, 8, 16):
+            prs.append(_gs_problem(m, n, k, 4, 4, seed=n + 3 * k + m)[0])
+    first = [o.clone() for o in P.gemm_grouped(prs)]
+    for _ in range(5):
+        for a, b in zip(first, P.gemm_grouped(prs)):
+            assert torch.equal(a.view(torch.int16), b.view(torch.int16))

@@ -12,10 +12,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2508_19087_b200 as P  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "W1A2"
-wb, ab = {"W1A2": (1, 2), "W2A2": (2, 2), "W3A4": (3, 4), "W4A4": (4, 4)}[which]
+PREC = {"W1A2": (1, 2), "W2A2": (2, 2), "W3A4": (3, 4), "W4A4": (4, 4)}
+precs = list(PREC.values()) if which == "all" else [PREC[which]]
+wb = max(p[0] for p in precs)
 dev = torch.device("cuda:0")
 probs = []
-for (n, k) in [(4096, 4096), (11008, 4096), (4096, 11008)]:
+for (wb, ab) in precs:
+  for (n, k) in [(4096, 4096), (11008, 4096), (4096, 11008)]:
     for m in (1, 8, 16):
         w = torch.randint(-(1 << (wb - 1)), 1 << (wb - 1), (n, k), dtype=torch.int8, device=dev)
         a = torch.randint(-(1 << (ab - 1)), 1 << (ab - 1), (m, k), dtype=torch.int8, device=dev)
@@ -35,6 +38,7 @@ torch.cuda.synchronize()
 buf = np.zeros((1024, 48, 4), dtype=np.uint64)
 fn(buf.ctypes.data, 0)
 t = buf.astype(np.float64)
+wb = max(p[0] for p in precs)
 ctas = np.nonzero(t[:, 0, 0])[0]
 t0 = t[ctas][:, :, :][t[ctas] > 0].min()
 lat, comp, pw, gap = [], [], [], []
