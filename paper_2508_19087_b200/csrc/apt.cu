@@ -744,10 +744,27 @@ static apt_status grp_run(int32_t count, const apt_gemm_problem* problems, const
   ga.workers = (int32_t)workers;
   ga.total_blocks = blocks;
   ga.total_cost = cost;
-  for (int i = 0; i < count; ++i) {  // owner of each problem's last block (gemm_grp.cu grp_owner, same formula)
-    const apt::GrpProblem& q = ga.p[i];
-    const int64_t last = (int64_t)q.tiles * q.nb - 1;
-    ga.p[i].w_hi = (int32_t)((2 * q.cost0 + (2 * last + 1) * (int64_t)q.cost) * workers / (2 * cost));
+  // every worker's first block: the first block whose owner (midpoint rule, gemm_grp.cu grp_owner) is that
+  // worker; owners are non-decreasing along the blocks and take every value (workers * max cost <= total)
+  if (workers > apt::kGrpMaxWorkers || blocks >= (1ll << 32)) return APT_ERR_UNSUPPORTED;
+  {
+    int next = 0;
+    for (int i = 0; i < count && next < workers; ++i) {
+      apt::GrpProblem& q = ga.p[i];
+      const int64_t nblk = (int64_t)q.tiles * q.nb;
+      auto owner = [&](int64_t b) { return (int)((2 * q.cost0 + (2 * b + 1) * (int64_t)q.cost) * workers / (2 * cost)); };
+      q.w_hi = owner(nblk - 1);
+      while (next < workers && next <= q.w_hi) {
+        // smallest b with owner(b) >= next (binary search over the problem's blocks)
+        int64_t lo = 0, hi = nblk - 1;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) / 2;
+          if (owner(mid) >= next) hi = mid; else lo = mid + 1;
+        }
+        ga.wstart[next++] = (uint32_t)(q.blk0 + lo);
+      }
+    }
+    for (; next <= workers; ++next) ga.wstart[next] = (uint32_t)blocks;
   }
   ga.tickets = reinterpret_cast<uint32_t*>(workspace);
   ga.partials = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(workspace) + APT_WS_TICKET_BYTES);

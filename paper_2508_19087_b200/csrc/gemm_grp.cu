@@ -118,25 +118,18 @@ __device__ __forceinline__ int grp_owner(const GrpArgs& a, const GrpProblem& q, 
 
 // first block (problem p, local index i, global index gi) owned by a worker >= w; p = count if none
 __device__ void grp_find(const GrpArgs& a, int w, int& p_out, int64_t& i_out, int64_t& g_out) {
-  for (int p = 0; p < a.count; ++p) {
-    const GrpProblem& q = a.p[p];
-    const int64_t nblk = (int64_t)q.tiles * q.nb;
-    if (q.w_hi < w) continue;  // == grp_owner(a, q, nblk - 1), precomputed on the host
-    // owner(i) >= w  <=>  (2 cost0 + (2 i + 1) c) W >= 2 w T
-    const int64_t cW = (int64_t)q.cost * a.workers;
-    const int64_t num = 2 * (int64_t)w * a.total_cost - 2 * q.cost0 * a.workers;
-    int64_t i = num > cW ? (num - cW + 2 * cW - 1) / (2 * cW) : 0;
-    if (i > nblk - 1) i = nblk - 1;
-    while (i > 0 && grp_owner(a, q, i - 1) >= w) --i;
-    while (grp_owner(a, q, i) < w) ++i;
-    p_out = p;
-    i_out = i;
-    g_out = q.blk0 + i;
+  // the host computed every worker's first block with the same owner formula (apt.cu grp_run)
+  const int64_t g = a.wstart[w];
+  g_out = g;
+  int p = 0;
+  while (p + 1 < a.count && a.p[p + 1].blk0 <= g) ++p;
+  if (g >= a.total_blocks) {
+    p_out = a.count;
+    i_out = 0;
     return;
   }
-  p_out = a.count;
-  i_out = 0;
-  g_out = a.total_blocks;
+  p_out = p;
+  i_out = g - a.p[p].blk0;
 }
 
 // one output element to out and, in launches with peers (a separate instantiation: even an untaken peer

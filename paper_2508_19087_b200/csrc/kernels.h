@@ -138,12 +138,14 @@ struct GrpProblem {
   int64_t a_gs_ld;
   int32_t k_words, nb, tiles, wbits, cost;  // nb = Kpad / 256 blocks per row tile; tiles = ceil(N / 128)
 };
+constexpr int kGrpMaxWorkers = 1024;
 struct GrpArgs {
   int32_t count, workers;  // workers = warps of the grid; workers * max cost <= total_cost
   int64_t total_blocks, total_cost;
   int32_t* partials;       // [workers][2][16 x 32] int32
   uint32_t* tickets;       // [workers], zero before and after the call
   GrpProblem p[kGrpMax];
+  uint32_t wstart[kGrpMaxWorkers + 1];  // global index of each worker's first block (host-computed; [workers] = total)
 };
 int grp_wbmax_class(int wbmax);
 int grp_ctas_per_sm(int wbmax, bool gs);
