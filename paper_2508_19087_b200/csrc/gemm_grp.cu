@@ -63,15 +63,15 @@ __device__ __forceinline__ void grp_rebuild(const uint32_t* w, uint32_t (&o)[8])
 __device__ __forceinline__ int grp_shift(int wb) { return wb <= 2 ? 8 - wb : wb <= 4 ? 4 : 0; }
 
 #ifdef APT_GRP_TRACE
-// per-unit globaltimer timeline (profiling builds only): [cta][unit < 48][0 weights issued, 1 tokens
+// per-unit globaltimer timeline (profiling builds only): [cta][unit < 128][0 weights issued, 1 tokens
 // issued, 2 consumer warp 0 saw full, 3 consumer warp 0 released]
-__device__ unsigned long long g_grp_trace[1024][48][4];
+__device__ unsigned long long g_grp_trace[1024][128][4];
 __device__ __forceinline__ unsigned long long grp_gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define GRP_TRACE(u, ph) do { if ((u) < 48 && blockIdx.x < 1024) g_grp_trace[blockIdx.x][(u)][(ph)] = grp_gtimer(); } while (0)
+#define GRP_TRACE(u, ph) do { if ((u) < 128 && blockIdx.x < 1024) g_grp_trace[blockIdx.x][(u)][(ph)] = grp_gtimer(); } while (0)
 #else
 #define GRP_TRACE(u, ph) do { } while (0)
 #endif
@@ -660,9 +660,9 @@ cudaError_t launch_gemm_grp(const GrpArgs& a, int wbmax, int ctas, bool gs, bool
 #ifdef APT_GRP_TRACE
 extern "C" __attribute__((visibility("default"))) int apt_debug_grp_trace(unsigned long long* host, int reset) {
   if (reset) {
-    static unsigned long long zero[1024 * 48 * 4];
+    static unsigned long long zero[1024 * 128 * 4];
     return (int)cudaMemcpyToSymbol(apt::g_grp_trace, zero, sizeof(zero));
   }
-  return (int)cudaMemcpyFromSymbol(host, apt::g_grp_trace, sizeof(unsigned long long) * 1024 * 48 * 4);
+  return (int)cudaMemcpyFromSymbol(host, apt::g_grp_trace, sizeof(unsigned long long) * 1024 * 128 * 4);
 }
 #endif

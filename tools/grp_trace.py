@@ -35,7 +35,7 @@ fn(None, 1)
 torch.cuda.synchronize()
 P.gemm_grouped(probs, workspace=ws)
 torch.cuda.synchronize()
-buf = np.zeros((1024, 48, 4), dtype=np.uint64)
+buf = np.zeros((1024, 128, 4), dtype=np.uint64)
 fn(buf.ctypes.data, 0)
 t = buf.astype(np.float64)
 wb = max(p[0] for p in precs)
@@ -61,5 +61,35 @@ print("data latency issue->full ns (p10, med, p90)", q(lat))
 print("consumer full->release ns", q(comp))
 print("consumer idle release(u-1)->full(u) ns", q(gap))
 print("producer release(u-D)->issue(u) ns", q(pw))
+full_ctas = [c for c in ctas if np.count_nonzero(t[c, :, 3]) < t.shape[1]]
+ends = np.array([t[c, :, 3].max() for c in full_ctas]) - t0
+print("ctas with a complete trace", len(full_ctas), "end us p0/p10/p50/p90/p100",
+      [round(float(np.percentile(ends, q)) / 1e3, 1) for q in (0, 10, 50, 90, 100)])
 print("cta start (first issue) spread us", round((t[ctas, 0, 0].max() - t[ctas, 0, 0].min()) / 1e3, 2),
       "cta end spread us", round((max(t[c, :, 3].max() for c in ctas) - min(t[c, :, 3].max() for c in ctas)) / 1e3, 2))
+
+# ---- per-class unit cost fit: replicate the host's stream-K split (apt.cu grp_run, same cost formula),
+# count every CTA's units per (wbits, M) class, least-squares fit CTA busy time = sum_c n_c x_c
+def unit_cost(wb, m):  # apt.cu grp_run
+    return 4 * wb + (16 if m > 8 else 8)
+meta = []  # per problem: (wb, m, units, cost)
+for (pwb, pab) in precs:
+    for (n, k) in [(4096, 4096), (11008, 4096), (4096, 11008)]:
+        for m in (1, 8, 16):
+            units = -(-n // 128) * (k // 256)
+            meta.append((pwb, m, units, unit_cost(pwb, m)))
+T = sum(u * c for (_, _, u, c) in meta)
+cmax = max(c for (_, _, _, c) in meta)
+W = min(148 * 4, T // cmax)
+cls = sorted({(w, m) for (w, m, _, _) in meta})
+A = np.zeros((W, len(cls)))
+cost0 = 0
+for (pwb, m, units, c) in meta:
+    b = np.arange(units)
+    owner = ((2 * cost0 + (2 * b + 1) * c) * W) // (2 * T)
+    for o, cnt in zip(*np.unique(owner, return_counts=True)):
+        A[o, cls.index((pwb, m))] += cnt
+    cost0 += units * c
+busy = np.array([t[c, :, 3].max() - t[c, 0, 0] for c in ctas[:W]])
+x, *_ = np.linalg.lstsq(A[ctas[:W]] if len(ctas) >= W else A, busy, rcond=None)
+print("fitted ns per unit by (wbits, M):", {f"W{k[0]} M{k[1]}": round(float(v), 1) for k, v in zip(cls, x)})
