@@ -37,6 +37,8 @@ P.gemm_grouped(probs, workspace=ws)
 torch.cuda.synchronize()
 buf = np.zeros((1024, 128, 4), dtype=np.uint64)
 fn(buf.ctypes.data, 0)
+smid = buf[:, 127, 3].astype(np.int64) - 1
+buf[:, 127, :] = 0
 t = buf.astype(np.float64)
 wb = max(p[0] for p in precs)
 ctas = np.nonzero(t[:, 0, 0])[0]
@@ -65,6 +67,22 @@ full_ctas = [c for c in ctas if np.count_nonzero(t[c, :, 3]) < t.shape[1]]
 ends = np.array([t[c, :, 3].max() for c in full_ctas]) - t0
 print("ctas with a complete trace", len(full_ctas), "end us p0/p10/p50/p90/p100",
       [round(float(np.percentile(ends, q)) / 1e3, 1) for q in (0, 10, 50, 90, 100)])
+sm_end = {}
+for c in full_ctas:
+    sm_end[smid[c]] = max(sm_end.get(smid[c], 0), t[c, :, 3].max() - t0)
+se = np.array(list(sm_end.values()))
+print("SMs", len(se), "per-SM end us p0/p10/p50/p90/p100", [round(float(np.percentile(se, q)) / 1e3, 1) for q in (0, 10, 50, 90, 100)])
+by_sm = {}
+for c in ctas:
+    by_sm.setdefault(int(smid[c]), []).append(int(c))
+order = sorted(sm_end)
+print("per-SM end us by smid (groups of 8):", [round(float(np.mean([sm_end[i] for i in order[j:j + 8]])) / 1e3, 1) for j in range(0, len(order), 8)])
+busy_sm = {}
+for c in full_ctas:
+    busy_sm[int(smid[c])] = busy_sm.get(int(smid[c]), 0) + sum(
+        (t[c, u, 3] - t[c, u, 2]) for u in range(t.shape[1]) if t[c, u, 3] and t[c, u, 2])
+print("per-SM consumer busy (warp 0) us p0/p50/p100", [round(float(np.percentile(list(busy_sm.values()), q)) / 1e3, 1) for q in (0, 50, 100)])
+print("CTAs of SM 0..3:", [by_sm.get(i) for i in range(4)], "smid of CTAs 0..9:", [int(smid[c]) for c in range(10)])
 print("cta start (first issue) spread us", round((t[ctas, 0, 0].max() - t[ctas, 0, 0].min()) / 1e3, 2),
       "cta end spread us", round((max(t[c, :, 3].max() for c in ctas) - min(t[c, :, 3].max() for c in ctas)) / 1e3, 2))
 
