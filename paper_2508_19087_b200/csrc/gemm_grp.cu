@@ -215,6 +215,13 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
   (void)i1;
   if (gstart >= gend) return;
 
+#ifdef APT_GRP_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {  // the SM of the CTA (slot 127: beyond the traced units)
+    unsigned sm_;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
+    g_grp_trace[blockIdx.x][127][3] = sm_ + 1;
+  }
+#endif
   if (warp == 4) {
     // ---- producer (one lane): per unit, WB bulk copies of 4 KB (weight planes) + M row copies of 256 B
     // (token digits), completing on the slot's full barrier; the weights of the first D units are
