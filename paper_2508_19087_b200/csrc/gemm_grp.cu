@@ -50,7 +50,10 @@ struct GrpShape {
   static constexpr int kD = WBMAX <= 2 ? 4 : 2;  // 48 / 40 / 72 KB per CTA: 4 / 4 / 3 CTAs per SM
 #endif
   static constexpr int kBarOff = kD * kSlot;
-  static constexpr int kSmem = kBarOff + 2 * kD * 8 + 16;
+  // per consumer warp: the epilogue operands of its 32 rows / 16 tokens (w_rowsum, w_scale, a_rowsum,
+  // a_scale: 384 bytes), copied in at the start of every segment so the epilogue never waits on global memory
+  static constexpr int kEpiOff = (kBarOff + 2 * kD * 8 + 16 + 15) / 16 * 16;
+  static constexpr int kSmem = kEpiOff + 4 * 384;
 };
 
 template <int WB>
@@ -75,6 +78,10 @@ __device__ __forceinline__ unsigned long long grp_gtimer() {
 #else
 #define GRP_TRACE(u, ph) do { } while (0)
 #endif
+
+__device__ __forceinline__ void grp_cp4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
 
 __device__ __forceinline__ void grp_mma(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                         uint32_t b1) {
@@ -329,6 +336,23 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
     const uint32_t trow1 = trow0 + 8 * 128;
     const uint32_t woff = (uint32_t)((cw * 32 + g) * 16 + t * 4);
 
+    // epilogue operands of this segment's tile into the warp's area (asynchronous; waited for at the
+    // epilogue): lane l -> row n_w + l, tokens l < 16
+    const uint32_t epi_s = sbase + (uint32_t)(SH::kEpiOff + cw * 384);
+    float* epi_p = reinterpret_cast<float*>(smem + SH::kEpiOff + cw * 384);
+    if constexpr (!GS) {
+      const int nl = min(n_w + lane, q.e.N - 1);
+      grp_cp4(epi_s + lane * 4, q.e.w_rowsum + nl);
+      if (q.e.kind == 2) grp_cp4(epi_s + 128 + lane * 4, q.e.w_scale + nl);
+      if (lane < 16) {
+        const int ml = min(lane, q.e.M - 1);
+        grp_cp4(epi_s + 256 + lane * 4, q.e.a_rowsum + ml);
+        if (q.e.kind == 2 && q.e.a_scale) grp_cp4(epi_s + 320 + lane * 4, q.e.a_scale + ml);
+        else epi_p[80 + lane] = 1.f;
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+
     int acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = 0;
@@ -573,14 +597,19 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
       const EpilogueArgs& e = q.e;
       const bool f16 = e.kind == 2;
       const bool zp = f16 && (q.w_zero || q.a_zero);
+      // the segment's prefetched operands: rows [0, 32) at 0 / 128 (int / float), tokens at 256 / 320
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+      const int32_t* ep_rw = reinterpret_cast<const int32_t*>(epi_p);
+      const int32_t* ep_ra = reinterpret_cast<const int32_t*>(epi_p + 64);
       if (!narrow) {  // acc[4 qq + 2 h + c]: token g + 8h, weight row n_w + 8 qq + 2t + c
         int32_t ra[2];
         float as[2], az[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int m = min(g + 8 * h, e.M - 1);
-          ra[h] = __ldg(e.a_rowsum + m);
-          as[h] = (f16 && e.a_scale) ? __ldg(e.a_scale + m) : 1.f;
+          ra[h] = ep_ra[g + 8 * h];
+          as[h] = epi_p[80 + g + 8 * h];
           az[h] = (zp && q.a_zero) ? __ldg(q.a_zero + m) : 0.f;
         }
 #pragma unroll
@@ -588,8 +617,8 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int n = n_w + 8 * qq + 2 * t + c, nc = min(n, e.N - 1);
-            const int32_t rw = __ldg(e.w_rowsum + nc);
-            const float wsc = f16 ? __ldg(e.w_scale + nc) : 0.f;
+            const int32_t rw = ep_rw[8 * qq + 2 * t + c];
+            const float wsc = f16 ? epi_p[32 + 8 * qq + 2 * t + c] : 0.f;
             const float wz = (zp && q.w_zero) ? __ldg(q.w_zero + nc) : 0.f;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -601,8 +630,8 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int m = min(2 * t + c, e.M - 1);
-          ra[c] = __ldg(e.a_rowsum + m);
-          as[c] = (f16 && e.a_scale) ? __ldg(e.a_scale + m) : 1.f;
+          ra[c] = ep_ra[2 * t + c];
+          as[c] = epi_p[80 + 2 * t + c];
           az[c] = (zp && q.a_zero) ? __ldg(q.a_zero + m) : 0.f;
         }
 #pragma unroll
@@ -610,8 +639,8 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int n = n_w + 16 * P + g + 8 * h, nc = min(n, e.N - 1);
-            const int32_t rw = __ldg(e.w_rowsum + nc);
-            const float wsc = f16 ? __ldg(e.w_scale + nc) : 0.f;
+            const int32_t rw = ep_rw[16 * P + g + 8 * h];
+            const float wsc = f16 ? epi_p[32 + 16 * P + g + 8 * h] : 0.f;
             const float wz = (zp && q.w_zero) ? __ldg(q.w_zero + nc) : 0.f;
 #pragma unroll
             for (int c = 0; c < 2; ++c)
