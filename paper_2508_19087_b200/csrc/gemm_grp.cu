@@ -541,8 +541,11 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
     }
 
     // ---- the tile: whole (one CTA) or split (partials + ticket; the last CTA to arrive reduces)
+    // a tile this segment covers whole needs no owner lookup; a split tile finds its first / last owner
+    // in the range table (binary search over indexed parameter loads: only for split tiles)
+    const bool whole = b_in == 0 && seg == nb;
     const int64_t tfirst = (int64_t)tile * nb;
-    const int fw = grp_owner(a, q, tfirst), lw = grp_owner(a, q, tfirst + nb - 1);
+    const int fw = whole ? w : grp_owner(a, q, tfirst), lw = whole ? w : grp_owner(a, q, tfirst + nb - 1);
     bool epi = true;
     if (fw != lw) {
       // each consumer warp reduces its own 32-row slice: partial, warp barrier (orders the lanes' stores
