@@ -667,15 +667,16 @@ static apt_status grp_run(int32_t count, const apt_gemm_problem* problems, const
     if (kpad_of(K) * 255ll * 255ll >= (1ll << 32)) return APT_ERR_UNSUPPORTED;  // u * 2^s digits (gemm_dec.cu)
     apt::GrpProblem& q = ga.p[i];
     {
-      // token digit view [M][Kpad] u8: 128 x M boxes, 128-byte swizzle
+      // token digit view [M][Kpad] u8, 128-byte swizzle
       apt::PFN_encodeTiled_t enc = apt::tensor_map_encoder();
       if (!enc) return APT_ERR_CUDA;
       const cuuint64_t kp = (cuuint64_t)P.A.k_words * 32;
-      cuuint64_t dims[2] = {kp, (cuuint64_t)M};
-      cuuint64_t strides[1] = {kp};
-      cuuint32_t box[2] = {128, (cuuint32_t)M};
-      cuuint32_t es[2] = {1, 1};
-      if (enc(&q.tok, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, P.A.digits, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      // [Kpad / 128 chunks][M rows][128 bytes]; a box = the 2 chunks of a 256-element block x 8 / 16 rows
+      cuuint64_t dims[3] = {128, (cuuint64_t)M, kp / 128};
+      cuuint64_t strides[2] = {kp, 128};
+      cuuint32_t box[3] = {128, M <= 8 ? 8u : 16u, 2};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (enc(&q.tok, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, P.A.digits, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return APT_ERR_INVALID_ARGUMENT;
     }

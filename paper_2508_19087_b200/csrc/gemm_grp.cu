@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
       pps = q.w_pstride;
       pwp = q.wp;
       ptok = &q.tok;
-      ptx = (uint32_t)pwb * 4096u + (uint32_t)q.e.M * 256u;
+      ptx = (uint32_t)pwb * 4096u + 2u * (q.e.M <= 8 ? 8u : 16u) * 128u;  // (token rows >= M: the TMA zero fill)
     };
     load_problem();
     auto weights = [&](int slot) {
@@ -261,8 +261,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
     };
     auto tokens = [&](int slot) {
       const uint32_t dst = sbase + (uint32_t)(slot * SH::kSlot + SH::kTok);
-      tma_load_2d(dst, ptok, full(slot), pblk * 256, 0);
-      tma_load_2d(dst + 2048, ptok, full(slot), pblk * 256 + 128, 0);
+      tma_load_3d(dst, ptok, full(slot), 0, 0, pblk * 2);  // both 128-byte chunks of the block, one box
     };
     auto advance = [&]() {
       if (++pblk == pnb) {
@@ -334,6 +333,9 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
     // hold stale data; their products are never stored.
     const uint32_t trow0 = (uint32_t)(SH::kTok + g * 128);
     const uint32_t trow1 = trow0 + 8 * 128;
+    // the token box is [2 chunks][R rows][128 bytes], R = 8 (M <= 8) or 16: chunk 1 starts R lines later
+    // (a multiple of 8, so the 128-byte swizzle of line (chunk R + r) is r & 7 in both chunks)
+    const uint32_t tbox = (q.e.M <= 8 ? 8u : 16u) * 128u;
     const uint32_t woff = (uint32_t)((cw * 32 + g) * 16 + t * 4);
 
     // epilogue operands of this segment's tile into the warp's area (asynchronous; waited for at the
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(160, GS ? 2 : APT_GRP_MINB) gemm_grp_kernel(co
         uint4 tk0[4], tk1[4];  // [2 box + k]: word t (box 0) then word t + 4 (box 1), rows g / g + 8
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t ch = (uint32_t)((j >> 1) * 2048 + (((2 * t + (j & 1)) ^ g) * 16));  // (r & 7) == g
+          const uint32_t ch = (uint32_t)((j >> 1) * tbox + (((2 * t + (j & 1)) ^ g) * 16));  // (line & 7) == g
           asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(tk0[j].x), "=r"(tk0[j].y), "=r"(tk0[j].z), "=r"(tk0[j].w)
                        : "r"(sl + trow0 + ch));
           if (MT == 2)
