@@ -18,7 +18,7 @@
 //
 // CTA = 1 producer warp + 4 consumer warps.  The producer lane moves each unit into a ring slot with
 // one cp.async.bulk per weight plane (4 KB: a 128-row x 256-K block of the tile-major layout is
-// contiguous) and two 2-D TMA boxes of the activation digit view (M rows x 128 bytes, 128-byte swizzle),
+// contiguous) and one 3-D TMA box of the activation digit view (2 x 8/16 rows x 128 bytes, 128B swizzle),
 // completing on the slot's full mbarrier.  Consumer warp cw owns rows 32 cw .. 32 cw + 31 of the tile;
 // lane (g, t) = (lane / 4, lane % 4) takes words t and t + 4 of the block for BOTH operands (so K
 // agrees; conflict-free shared-memory reads), rebuilds the weight digits (rebuild_hi / rebuild_x16 /
@@ -40,8 +40,8 @@ template <int WBMAX>
 struct GrpShape {
   // CTA = 4 consumer warps (32 weight rows each) + 1 producer warp; unit = 128 weight rows x 256 K.
   // Slot = WBMAX weight planes of the unit (4 KB each: the tile-major [half][128 rows][4 words] block,
-  // one contiguous bulk copy per plane) + the unit's token digits (two 2-D TMA boxes of M rows x 128
-  // bytes, 128-byte swizzle: the fragment reads of rows g = 0..7 hit distinct banks).
+  // one contiguous bulk copy per plane) + the unit's token digits (one 3-D TMA box, 2 chunks x 8 / 16
+  // rows x 128 bytes, zero fill past M, 128-byte swizzle: the fragment reads of rows g = 0..7 hit distinct banks).
   static constexpr int kTok = WBMAX * 4096;
   static constexpr int kSlot = WBMAX * 4096 + 4096;
 #ifdef APT_GRP_D
