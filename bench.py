@@ -611,7 +611,8 @@ def run_legs(args, torch, P, dev, stream, world, rank, barrier, legs):
                              "cublas_int8_us": round(int8_us, 2), "cublas_fp16_us": round(fp16_us, 2),
                              "speedup_vs_int8": round(int8_us / us, 3), "speedup_vs_fp16": round(fp16_us / us, 3),
                              "tensor_frac": round(tops / (peak * (2 if mx else 1)), 4),
-                             "kernel": "tcgen05 kind::mxf4" if mx else "tcgen05 kind::i8", "bn": cfg["bn"]})
+                             "kernel": ("persistent " if cfg["kernel"] == 6 else "") +
+                                       ("tcgen05 kind::mxf4" if mx else "tcgen05 kind::i8"), "bn": cfg["bn"]})
         tot_ops = sum(2 * 2048 * n * k for _ in range(2) for (n, k) in SHAPES)
         tot_us = sum(r["us"] for r in rows)
         out["prefill"] = {"workload": "BASELINE configs[2]: Llama-2-7B prefill M=2048, W2A8 and W4A4",
@@ -661,7 +662,8 @@ def run_legs(args, torch, P, dev, stream, world, rank, barrier, legs):
                          "gemm_gather_us": round(gather_us, 2) if gather_us else None,
                          "gemm_gather_eff_tops": round(ops / gather_us / 1e6, 1) if gather_us else None,
                          "ingress_bound_us": round(ingress_us, 1) if ingress_us else None,
-                         "kernel": "tcgen05 kind::mxf4" if cfg["mma_kind"] == 1 else "tcgen05 kind::i8"})
+                         "kernel": ("persistent " if cfg["kernel"] == 6 else "") +
+                                   ("tcgen05 kind::mxf4" if cfg["mma_kind"] == 1 else "tcgen05 kind::i8")})
         out["llama70b_tp"] = {"workload": f"BASELINE configs[3]: Llama-3-70B linears M=4096 W2A4, N-split over {world} "
                                           "GPU(s), column-layout slices, NCCL all-gather of 4 M-chunks overlapped "
                                           "with the next chunk's GEMM (N>1)",

@@ -66,9 +66,11 @@ apt_status validate_config(const apt_config* c, int32_t M, int32_t N, int32_t K,
   if (c->w_digit != wbits || c->a_digit != abits) return APT_ERR_UNSUPPORTED;  // full-width digits only
   if (c->mma_kind != APT_MMA_I8 && c->mma_kind != APT_MMA_MXF4) return APT_ERR_UNSUPPORTED;
   if (c->kernel == APT_KERNEL_PF) {
-    if (c->bm != 128 || c->bn != 128 || c->bk != 128 || c->stages != 6 || c->split_k != 1 || c->cluster_n != 1 ||
-        c->cta_pair != 0)
+    if (c->bm != 128 || (c->bn != 128 && c->bn != 192 && c->bn != 256) || c->bk != 128 ||
+        c->stages != (c->bn == 128 ? 6 : c->bn == 192 ? 4 : 3) || c->split_k != 1 || c->cluster_n != 1 || c->cta_pair != 0)
       return APT_ERR_UNSUPPORTED;
+    // 2 x 192 accumulator + A ring = 512 TMEM columns; 2 x 256 with the A ring in shared memory: i8 only
+    if (c->bn != 128 && c->mma_kind != APT_MMA_I8) return APT_ERR_UNSUPPORTED;
     if (c->mma_kind == APT_MMA_MXF4 && (wbits > 3 || abits > 3 || kpad_of(K) * 16ll >= (1ll << 24)))
       return APT_ERR_UNSUPPORTED;
     // i8: weight digits scaled by 2^s (<= 255 each) accumulate in s32: Kpad * 255 * 255 < 2^31
@@ -351,13 +353,20 @@ apt_status select_analytic(int32_t M, int32_t N, int32_t K, int32_t wbits, int32
   out->bk = 128;
   out->cta_pair = 0;
   if (M > 64) {
-    // prefill: 128 weight rows x 256 tokens per CTA, one CTA per SM, no cluster.  The weight rebuild
-    // (converter warps, integer ALU) is paid once per 256 tokens instead of 128; measured on B200
-    // (profiles/r1_prefill_bn_sweep.txt) 1.0-1.4x faster than 2 x (128 x 128) CTAs per SM with the
-    // token tile multicast to a 4-CTA cluster, and faster than the 256-token tile in 2-CTA clusters
+    // token-rich: 128 weight rows x 256 tokens per tile, no cluster.  The weight rebuild (converter
+    // warps, integer ALU) is paid once per 256 tokens instead of 128 (profiles/r1_prefill_bn_sweep.txt:
+    // 1.0-1.4x faster than 2 x (128 x 128) CTAs per SM with a 4-CTA token multicast).  The persistent
+    // tile (one CTA per SM walking the tiles, epilogue overlapped with the next tile's MMAs) where its
+    // s32 accumulation of scaled digits is exact: 0.95-1.25x the one-tile-per-CTA kernel on the
+    // prefill, Llama-3-70B and sweep shapes (profiles/r2_pf256_ab.jsonl)
     out->bn = 256;
     out->split_k = 1;
     out->cluster_n = 1;
+    if (kpad_of(K) * 255ll * 255ll < (1ll << 31)) {
+      out->kernel = APT_KERNEL_PF;
+      out->stages = 3;
+      return APT_OK;
+    }
   } else if (M <= 2) {
     // one or two tokens: the SIMT dp4a GEMV (SURVEY §8 a9 "pick by measurement"; 1.2-2.2x faster
     // than the tensor-core decode tile on every Llama-2-7B decode linear at M = 1, 2).
@@ -604,13 +613,14 @@ int32_t apt_enumerate_configs(int32_t M, int32_t N, int32_t K, int32_t wbits, in
   for (int bn : {16, 64, 128, 256})
     for (int cn : {1, 2, 4})
       for (int sp = 1; sp <= 8; ++sp) add(APT_KERNEL_TC, 128, bn, 128, apt::tc_stages(wbits, bn), sp, cn);
-  for (int mk : {APT_MMA_I8, APT_MMA_MXF4}) {  // the persistent tile
-    apt_config c;
-    std::memset(&c, 0, sizeof(c));
-    c.kernel = APT_KERNEL_PF; c.w_digit = wbits; c.a_digit = abits; c.bm = 128; c.bn = 128; c.bk = 128;
-    c.stages = 6; c.split_k = 1; c.cluster_n = 1; c.mma_kind = mk;
-    if (validate_config(&c, M, N, K, wbits, abits) == APT_OK) v.push_back(c);
-  }
+  for (int bn : {128, 192, 256})  // the persistent tile
+    for (int mk : {APT_MMA_I8, APT_MMA_MXF4}) {
+      apt_config c;
+      std::memset(&c, 0, sizeof(c));
+      c.kernel = APT_KERNEL_PF; c.w_digit = wbits; c.a_digit = abits; c.bm = 128; c.bn = bn; c.bk = 128;
+      c.stages = bn == 128 ? 6 : bn == 192 ? 4 : 3; c.split_k = 1; c.cluster_n = 1; c.mma_kind = mk;
+      if (validate_config(&c, M, N, K, wbits, abits) == APT_OK) v.push_back(c);
+    }
   for (int bn : {128, 256}) {  // kind::mxf4 (wbits, abits <= 3)
     apt_config c;
     std::memset(&c, 0, sizeof(c));
@@ -863,7 +873,7 @@ apt_status launch_product(const apt_config& c, const apt_packed* W, const apt_pa
       p.e.h_w = 0;
       p.e.h_a = 0;
     }
-    return apt::launch_gemm_pf(p, wbits, mx ? 1 : 0, s) == cudaSuccess ? APT_OK : APT_ERR_CUDA;
+    return apt::launch_gemm_pf(p, wbits, mx ? 1 : 0, c.bn, s) == cudaSuccess ? APT_OK : APT_ERR_CUDA;
   }
   if (c.mma_kind == APT_MMA_MXF4) {
     // kind::mxf4: tokens as signed e2m1 nibbles, expanded from the activation planes into the workspace;

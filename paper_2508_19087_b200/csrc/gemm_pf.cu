@@ -29,32 +29,45 @@
 namespace apt {
 
 constexpr int kPfBM = 128;  // weight rows per tile (MMA M)
-constexpr int kPfBN = 128;  // tokens per tile (MMA N)
 #ifndef APT_PF_CONV_PAR
 #define APT_PF_CONV_PAR 2  // converter warps per TMEM sub-partition (steps alternate between them)
 #endif
 constexpr int kPfConvPar = APT_PF_CONV_PAR;
+#ifndef APT_PF256_AS
+#define APT_PF256_AS 2  // shared-memory A stages of the 256-token tile
+#endif
 constexpr int kPfEpiWarp0 = 4 + 4 * kPfConvPar;       // first epilogue warp
 constexpr int kPfThreads = 32 * (kPfEpiWarp0 + 4);
 
-template <int WB, bool MX>
+// BN = tokens per tile (MMA N): 128; 192 (i8 only) — 2 x 192 accumulator columns + the 4 x 32 A ring fill
+// the 512 TMEM columns; 256 (i8 only) — the two accumulators take all 512 columns, so the converters
+// write the rebuilt weight digits to a shared-memory A ring (128-byte swizzled K-major rows, the layout
+// the token TMA boxes have) and the MMAs read both operands through descriptors
+template <int WB, bool MX, int BN>
 struct PfSmem {
-  static constexpr int kTokStages = 6;
-  static constexpr int kBBytes = kPfBN * 128;  // token bytes per step: 128 rows x 128 B (i8 128 K / mxf4 256 K)
+  static constexpr bool kASmem = BN == 256;
+  static constexpr int kBBytes = BN * 128;  // token bytes per step: 128 rows x 128 B (i8 128 K / mxf4 256 K)
   static constexpr int kWChunk = WB * 4096;    // weight bytes per 256-K chunk, every plane
-  static constexpr int kWSlots = WB <= 2 ? 8 : WB <= 4 ? 6 : 3;
-  static constexpr int kAStages = 4;
+  static constexpr int kWSlots = kASmem ? (WB <= 2 ? 4 : WB <= 4 ? 3 : 2) : (WB <= 2 ? 8 : WB <= 4 ? 6 : 3);
+  static constexpr int kAStages = kASmem ? APT_PF256_AS : 4;
+  static constexpr int kABytes = kPfBM * 128;  // one A stage in shared memory: 128 rows x 128 K bytes
+  // 256-token tiles: as many token stages as the rest of the 227 KB leaves (the token ring hides the L2
+  // latency of the 32 KB boxes; 3 stages starve the MMAs)
+  static constexpr int kTokFit = (225 * 1024 - kAStages * kABytes - kWSlots * kWChunk) / kBBytes;
+  static constexpr int kTokStages = BN <= 128 ? 6 : BN <= 192 ? 4 : (kTokFit < 6 ? kTokFit : 6);
   static constexpr int kBOff = 0;
   static constexpr int kWOff = kTokStages * kBBytes;
-  static constexpr int kBarOff = kWOff + kWSlots * kWChunk;
+  static constexpr int kAOff = kWOff + kWSlots * kWChunk;
+  static constexpr int kBarOff = kAOff + (kASmem ? kAStages * kABytes : 0);
   static constexpr int kNumBars = 2 * kTokStages + 2 * kWSlots + 2 * kAStages + 4;
   static constexpr int kTotal = kBarOff + kNumBars * 8 + 16 + 1024;  // + TMEM slot + alignment slack
 };
 
-template <int WB, bool MX>
+template <int WB, bool MX, int BN>
 __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_constant__ CUtensorMap tm_w,
                                                                const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
-  using L = PfSmem<WB, MX>;
+  static_assert(BN == 128 || ((BN == 192 || BN == 256) && !MX), "token tile");
+  using L = PfSmem<WB, MX, BN>;
   constexpr int ST = L::kTokStages, WS = L::kWSlots, AS = L::kAStages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -70,12 +83,12 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
   auto acc_full = [&](int b) { return bars + 8u * (2 * ST + 2 * WS + 2 * AS + b); };
   auto acc_empty = [&](int b) { return bars + 8u * (2 * ST + 2 * WS + 2 * AS + 2 + b); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L::kBarOff + L::kNumBars * 8);
-  constexpr uint32_t kAcol0 = 2 * kPfBN;         // A ring after the two accumulator buffers
+  constexpr uint32_t kAcol0 = 2 * BN;         // A ring after the two accumulator buffers
   constexpr uint32_t kScol0 = kAcol0 + 32 * AS;  // mxf4 unit scale factors
   constexpr int kShift = MX ? 0 : WB <= 2 ? 8 - WB : WB <= 4 ? 4 : 0;  // i8 weight digits are u * 2^kShift
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  const int tiles_n = (p.e.N + kPfBM - 1) / kPfBM, tiles_m = (p.e.M + kPfBN - 1) / kPfBN;
+  const int tiles_n = (p.e.N + kPfBM - 1) / kPfBM, tiles_m = (p.e.M + BN - 1) / BN;
   const int tiles = tiles_n * tiles_m;
   const int chunks = p.k_words >> 3;                  // 256-element weight chunks per tile
   const int nsteps = MX ? chunks : 2 * chunks;         // MMA steps per tile
@@ -145,7 +158,7 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
             const int s = gs % ST;
             mbar_wait(empty(s), ((gs / ST) & 1) ^ 1);
             mbar_expect_tx(full(s), (uint32_t)L::kBBytes);
-            tma_load_2d(sB + s * L::kBBytes, &tm_b, full(s), (MX ? c : 2 * c + h) * 128, tm * kPfBN);
+            tma_load_2d(sB + s * L::kBBytes, &tm_b, full(s), (MX ? c : 2 * c + h) * 128, tm * BN);
           }
         }
       }
@@ -153,24 +166,27 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = MX ? ((1u << 7) | (1u << 10) | ((uint32_t)(kPfBN >> 3) << 17) | (1u << 23) |
+      constexpr uint32_t idesc = MX ? ((1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) |
                                        ((uint32_t)(kPfBM >> 4) << 24))
-                                    : ((2u << 4) | ((uint32_t)(kPfBN >> 3) << 17) | ((uint32_t)(kPfBM >> 4) << 24));
+                                    : ((2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kPfBM >> 4) << 24));
       int gs = 0, li = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++li) {
         const int buf = li & 1;
         mbar_wait(acc_empty(buf), ((li >> 1) & 1) ^ 1);  // the epilogue of tile li - 2 released it
         tc_fence_after();
-        const uint32_t dcol = tmem + (uint32_t)(buf * kPfBN);
+        const uint32_t dcol = tmem + (uint32_t)(buf * BN);
         for (int j = 0; j < nsteps; ++j, ++gs) {
           const int s = gs % ST, a = gs % AS;
           mbar_wait(full(s), (gs / ST) & 1);
           mbar_wait(a_full(a), (gs / AS) & 1);
           tc_fence_after();
           const uint64_t bdesc = umma_desc_sw128(sB + s * L::kBBytes);
+          const uint64_t adesc = umma_desc_sw128(base + L::kAOff + a * L::kABytes);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            if constexpr (MX)
+            if constexpr (L::kASmem)
+              tc_mma_i8_ss(dcol, adesc + (uint64_t)(2 * kk), bdesc + (uint64_t)(2 * kk), idesc, (j | kk) != 0);
+            else if constexpr (MX)
               tc_mma_mxf4(dcol, tmem + kAcol0 + 32 * a + 8 * kk, bdesc + (uint64_t)(2 * kk), idesc, (j | kk) != 0,
                           tmem + kScol0, tmem + kScol0 + 16);
             else
@@ -247,12 +263,23 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
       }
       const int a = gs % AS;
       mbar_wait(a_empty(a), ((gs / AS) & 1) ^ 1);
-      tc_fence_after();
-      tmem_st32<32>(tmem + lane_off + kAcol0 + 32 * a, d);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_full(a));
+      if constexpr (L::kASmem) {
+        // row r of the stage: 16-byte chunk c (TMEM columns 4c .. 4c + 3, K bytes 16c ..) at chunk c ^ (r % 8)
+        uint8_t* arow = gbase + L::kAOff + a * L::kABytes + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(arow + ((c ^ (r & 7)) << 4)) = make_uint4(d[4 * c], d[4 * c + 1], d[4 * c + 2], d[4 * c + 3]);
+        fence_proxy_async();  // the generic-proxy stores, before the MMA's async-proxy reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full(a));
+      } else {
+        tc_fence_after();
+        tmem_st32<32>(tmem + lane_off + kAcol0 + 32 * a, d);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full(a));
+      }
     }
   } else if (warp >= kPfEpiWarp0) {
     // ------------------------------------------------------------ epilogue
@@ -260,11 +287,12 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
     const int r = ew * 32 + lane;
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     pdl_wait();  // token row sums / scales and the output may be touched by the previous kernel
+    const bool vec_tok = p.e.a_scale && ((reinterpret_cast<uintptr_t>(p.e.a_rowsum) | reinterpret_cast<uintptr_t>(p.e.a_scale)) & 15u) == 0;
     int li = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++li) {
       const int buf = li & 1;
       const int tn = t / tiles_m, tm = t % tiles_m;
-      const int n = tn * kPfBM + r, m0 = tm * kPfBN;
+      const int n = tn * kPfBM + r, m0 = tm * BN;
       const int nc = min(n, p.e.N - 1);
       const int32_t rw = __ldg(p.e.w_rowsum + nc);
       const float wsc = p.e.kind == 2 ? __ldg(p.e.w_scale + nc) : 0.f;
@@ -272,9 +300,9 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
       mbar_wait(acc_full(buf), (li >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < kPfBN; c0 += 32) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t acc[32];
-        tmem_ld32(tmem + lane_off + (uint32_t)(buf * kPfBN + c0), acc);
+        tmem_ld32(tmem + lane_off + (uint32_t)(buf * BN + c0), acc);
         if constexpr (MX) {
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) acc[jj] = (uint32_t)__float2int_rn(__uint_as_float(acc[jj]));
@@ -287,16 +315,35 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
           // nothing of this chunk is stored by this lane
         } else if (p.e.kind == 2) {
           uint32_t hv[16];
+          if (vec_tok && mb + 32 <= p.e.M) {
+            // the chunk's 32 token row sums / scales as 16-byte loads (same values for every lane)
 #pragma unroll
-          for (int jj = 0; jj < 32; jj += 2) {
-            float v2[2];
+            for (int j4 = 0; j4 < 32; j4 += 4) {
+              const int4 ra4 = __ldg(reinterpret_cast<const int4*>(p.e.a_rowsum + mb + j4));
+              const float4 as4 = __ldg(reinterpret_cast<const float4*>(p.e.a_scale + mb + j4));
+              const int32_t rr[4] = {ra4.x, ra4.y, ra4.z, ra4.w};
+              const float aa[4] = {as4.x, as4.y, as4.z, as4.w};
+              float v4[4];
 #pragma unroll
-            for (int e2 = 0; e2 < 2; ++e2) {
-              const int m = min(mb + jj + e2, p.e.M - 1);
-              const uint32_t y = acc[jj + e2] - (uint32_t)p.e.h_w * (uint32_t)__ldg(p.e.a_rowsum + m) - cn;
-              v2[e2] = ((float)(int32_t)y * wsc) * (p.e.a_scale ? __ldg(p.e.a_scale + m) : 1.f);
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t y = acc[j4 + e] - (uint32_t)p.e.h_w * (uint32_t)rr[e] - cn;
+                v4[e] = ((float)(int32_t)y * wsc) * aa[e];
+              }
+              hv[j4 / 2] = pack_f16x2(v4[0], v4[1]);
+              hv[j4 / 2 + 1] = pack_f16x2(v4[2], v4[3]);
             }
-            hv[jj / 2] = pack_f16x2(v2[0], v2[1]);
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 32; jj += 2) {
+              float v2[2];
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2) {
+                const int m = min(mb + jj + e2, p.e.M - 1);
+                const uint32_t y = acc[jj + e2] - (uint32_t)p.e.h_w * (uint32_t)__ldg(p.e.a_rowsum + m) - cn;
+                v2[e2] = ((float)(int32_t)y * wsc) * (p.e.a_scale ? __ldg(p.e.a_scale + m) : 1.f);
+              }
+              hv[jj / 2] = pack_f16x2(v2[0], v2[1]);
+            }
           }
           unsigned short* outh = reinterpret_cast<unsigned short*>(p.e.out);
           if (p.e.layout == 0) {
@@ -340,20 +387,21 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
   }
 }
 
-template <int WB, bool MX>
+template <int WB, bool MX, int BN>
 static cudaError_t launch_pf2(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, cudaStream_t stream) {
-  using L = PfSmem<WB, MX>;
+  using L = PfSmem<WB, MX, BN>;
   static_assert(L::kTotal <= 227 * 1024, "shared memory budget");
-  cudaError_t err = set_smem_once<gemm_pf_kernel<WB, MX>>(L::kTotal);
+  cudaError_t err = set_smem_once<gemm_pf_kernel<WB, MX, BN>>(L::kTotal);
   if (err != cudaSuccess) return err;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = ((p.e.N + kPfBM - 1) / kPfBM) * ((p.e.M + kPfBN - 1) / kPfBN);
+  const int tiles = ((p.e.N + kPfBM - 1) / kPfBM) * ((p.e.M + BN - 1) / BN);
   const int grid = tiles < sms ? tiles : sms;
-  return launch_pdl(gemm_pf_kernel<WB, MX>, dim3(grid), dim3(kPfThreads), L::kTotal, stream, dim3(1, 1, 1), tw, tb, p);
+  return launch_pdl(gemm_pf_kernel<WB, MX, BN>, dim3(grid), dim3(kPfThreads), L::kTotal, stream, dim3(1, 1, 1), tw, tb, p);
 }
 
-cudaError_t launch_gemm_pf(const TcArgs& p, int wbits, int mx, cudaStream_t stream) {
+cudaError_t launch_gemm_pf(const TcArgs& p, int wbits, int mx, int bn, cudaStream_t stream) {
+  if (bn != 128 && ((bn != 192 && bn != 256) || mx)) return cudaErrorInvalidValue;
   PFN_encodeTiled_t enc = tensor_map_encoder();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tw, tb;
@@ -362,7 +410,7 @@ cudaError_t launch_gemm_pf(const TcArgs& p, int wbits, int mx, cudaStream_t stre
     const cuuint64_t kp = (cuuint64_t)p.k_words * (mx ? 16 : 32);
     cuuint64_t dims[2] = {kp, (cuuint64_t)p.e.M};
     cuuint64_t strides[1] = {kp};
-    cuuint32_t box[2] = {128u, (cuuint32_t)kPfBN};
+    cuuint32_t box[2] = {128u, (cuuint32_t)bn};
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(p.adig), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -371,21 +419,45 @@ cudaError_t launch_gemm_pf(const TcArgs& p, int wbits, int mx, cudaStream_t stre
   }
   if (mx) {
     switch (wbits) {
-      case 1: return launch_pf2<1, true>(tw, tb, p, stream);
-      case 2: return launch_pf2<2, true>(tw, tb, p, stream);
-      case 3: return launch_pf2<3, true>(tw, tb, p, stream);
+      case 1: return launch_pf2<1, true, 128>(tw, tb, p, stream);
+      case 2: return launch_pf2<2, true, 128>(tw, tb, p, stream);
+      case 3: return launch_pf2<3, true, 128>(tw, tb, p, stream);
       default: return cudaErrorInvalidValue;
     }
   }
+  if (bn == 256) {
+    switch (wbits) {
+      case 1: return launch_pf2<1, false, 256>(tw, tb, p, stream);
+      case 2: return launch_pf2<2, false, 256>(tw, tb, p, stream);
+      case 3: return launch_pf2<3, false, 256>(tw, tb, p, stream);
+      case 4: return launch_pf2<4, false, 256>(tw, tb, p, stream);
+      case 5: return launch_pf2<5, false, 256>(tw, tb, p, stream);
+      case 6: return launch_pf2<6, false, 256>(tw, tb, p, stream);
+      case 7: return launch_pf2<7, false, 256>(tw, tb, p, stream);
+      default: return launch_pf2<8, false, 256>(tw, tb, p, stream);
+    }
+  }
+  if (bn == 192) {
+    switch (wbits) {
+      case 1: return launch_pf2<1, false, 192>(tw, tb, p, stream);
+      case 2: return launch_pf2<2, false, 192>(tw, tb, p, stream);
+      case 3: return launch_pf2<3, false, 192>(tw, tb, p, stream);
+      case 4: return launch_pf2<4, false, 192>(tw, tb, p, stream);
+      case 5: return launch_pf2<5, false, 192>(tw, tb, p, stream);
+      case 6: return launch_pf2<6, false, 192>(tw, tb, p, stream);
+      case 7: return launch_pf2<7, false, 192>(tw, tb, p, stream);
+      default: return launch_pf2<8, false, 192>(tw, tb, p, stream);
+    }
+  }
   switch (wbits) {
-    case 1: return launch_pf2<1, false>(tw, tb, p, stream);
-    case 2: return launch_pf2<2, false>(tw, tb, p, stream);
-    case 3: return launch_pf2<3, false>(tw, tb, p, stream);
-    case 4: return launch_pf2<4, false>(tw, tb, p, stream);
-    case 5: return launch_pf2<5, false>(tw, tb, p, stream);
-    case 6: return launch_pf2<6, false>(tw, tb, p, stream);
-    case 7: return launch_pf2<7, false>(tw, tb, p, stream);
-    default: return launch_pf2<8, false>(tw, tb, p, stream);
+    case 1: return launch_pf2<1, false, 128>(tw, tb, p, stream);
+    case 2: return launch_pf2<2, false, 128>(tw, tb, p, stream);
+    case 3: return launch_pf2<3, false, 128>(tw, tb, p, stream);
+    case 4: return launch_pf2<4, false, 128>(tw, tb, p, stream);
+    case 5: return launch_pf2<5, false, 128>(tw, tb, p, stream);
+    case 6: return launch_pf2<6, false, 128>(tw, tb, p, stream);
+    case 7: return launch_pf2<7, false, 128>(tw, tb, p, stream);
+    default: return launch_pf2<8, false, 128>(tw, tb, p, stream);
   }
 }
 

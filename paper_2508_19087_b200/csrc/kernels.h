@@ -57,7 +57,7 @@ struct TcArgs {
 cudaError_t launch_gemm_tc(const TcArgs& p, int wbits, int bn, int cluster_n, int split, int mx, cudaStream_t stream);
 // persistent tcgen05 GEMM (gemm_pf.cu): 128 x 128 tiles walked by one CTA per SM, double-buffered
 // accumulator; mx = kind::mxf4 (tokens = the e2m1 view)
-cudaError_t launch_gemm_pf(const TcArgs& p, int wbits, int mx, cudaStream_t stream);
+cudaError_t launch_gemm_pf(const TcArgs& p, int wbits, int mx, int bn, cudaStream_t stream);
 // activation planes -> signed e2m1 token view [M][Kpad / 2] for the kind::mxf4 path (abits <= 3)
 cudaError_t launch_expand_tokens_mx(const uint32_t* ap, int64_t a_pstride, int M, int k_words, int abits, uint8_t* out,
                                     cudaStream_t stream);

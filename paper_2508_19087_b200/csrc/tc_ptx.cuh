@@ -30,6 +30,17 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint32_t a_tmem, uint
       : "memory");
 }
 
+// A and B both from shared memory (descriptors)
+__device__ __forceinline__ void tc_mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
 // SMEM matrix descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart (SBO),
 // version 1 (sm_100), base offset 0 (stage buffers are 1024-byte aligned).
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {

@@ -85,7 +85,9 @@ def test_selector_legal_and_deterministic(M, N, K, wb, ab, table_mode):
         if table_mode == "analytic":
             assert 2 < M <= 8 and K <= 4096 and c.bn == 8 and c.split_k in (4, 8)
     elif c.kernel == L.APT_KERNEL_PF:
-        assert table_mode == "table" and c.bm == 128 and c.bn == 128 and c.split_k == 1 and c.cluster_n == 1
+        assert c.bm == 128 and c.bn in (128, 192, 256) and c.split_k == 1 and c.cluster_n == 1 and M > 2
+        if table_mode == "analytic":  # token-rich shapes: the persistent 256-token tile
+            assert M > 64 and c.bn == 256 and c.stages == 3 and c.mma_kind == L.APT_MMA_I8
     elif c.kernel == L.APT_KERNEL_DEC:
         assert table_mode == "table" and M <= 16 and c.bm == 32 and c.bn == (8 if M <= 8 else 16) and c.bk == 256
         assert c.stages in (4, 8) and 1 <= c.split_k <= 32 and c.cluster_n == 1 and c.cta_pair == 0

@@ -231,7 +231,7 @@ def test_config_invariance_tc(bn, cn, split, wb, ab):
     a = signed_codes(300, 3000, ab, seed=5)
     w = signed_codes(600, 3000, wb, seed=6)
     cfg = P.select_config(300, 600, 3000, wb, ab)
-    cfg.update(bn=bn, cluster_n=cn, split_k=split, stages=_tc_stages(wb, bn))
+    cfg.update(kernel=2, bn=bn, cluster_n=cn, split_k=split, stages=_tc_stages(wb, bn))
     _check_gemm(a, ab, w, wb, config=cfg)
 
 
@@ -740,14 +740,17 @@ def test_ablation_basic_plane_pairs(m, n, k, pw, pa):
 
 # ----------------------------------------------------------------------------- persistent tcgen05 tile (APT_KERNEL_PF)
 
-def _pf_cfg(m, n, k, wb, ab, mx=0):
-    return dict(P.select_config(m, n, k, wb, ab), kernel=6, bm=128, bn=128, bk=128, stages=6, split_k=1, cta_pair=0,
-                cluster_n=1, mma_kind=mx)
+def _pf_cfg(m, n, k, wb, ab, mx=0, bn=128):
+    return dict(P.select_config(m, n, k, wb, ab), kernel=6, bm=128, bn=bn, bk=128, stages={128: 6, 192: 4, 256: 3}[bn],
+                split_k=1, cta_pair=0, cluster_n=1, mma_kind=mx)
 
 
-@pytest.mark.parametrize("pw,pa,mx", [(1, 1, 0), (2, 8, 0), (4, 4, 0), (5, 3, 0), (8, 8, 0), (3, 3, 1), (1, 2, 1), (2, 3, 1)])
+@pytest.mark.parametrize("pw,pa,mx,bn", [(1, 1, 0, 128), (2, 8, 0, 128), (4, 4, 0, 128), (5, 3, 0, 128), (8, 8, 0, 128),
+                                         (3, 3, 1, 128), (1, 2, 1, 128), (2, 3, 1, 128),
+                                         (1, 1, 0, 192), (2, 8, 0, 192), (4, 4, 0, 192), (5, 3, 0, 192), (8, 8, 0, 192),
+                                         (1, 1, 0, 256), (2, 8, 0, 256), (4, 4, 0, 256), (5, 3, 0, 256), (8, 8, 0, 256)])
 @pytest.mark.parametrize("tiled", [True, False])
-def test_pf_matches_oracle(pw, pa, mx, tiled):
+def test_pf_matches_oracle(pw, pa, mx, bn, tiled):
     """APT_KERNEL_PF (i8 and mxf4): int32 signed / bipolar bit-exact and fp16 within 1e-3 on ragged shapes
     (M, N not multiples of 128, K not a multiple of 256, more tiles than SMs and fewer), row and column
     layouts, tile-major and canonical weights, with and without the activation digit view."""
@@ -756,7 +759,7 @@ def test_pf_matches_oracle(pw, pa, mx, tiled):
         w = signed_codes(n, k, pw, seed=520 + pw + n)
         A = P.pack(_dev(a), pa, digits=(m % 2 == 0))
         W = P.pack(_dev(w), pw, tiled=tiled)
-        cfg = _pf_cfg(m, n, k, pw, pa, mx)
+        cfg = _pf_cfg(m, n, k, pw, pa, mx, bn)
         ref = O.gemm_signed(a, w)
         assert np.array_equal(P.gemm(W, A, config=cfg).cpu().numpy().astype(np.int64), ref)
         got = P.gemm(W, A, out_kind="bipolar", layout="col", config=cfg).cpu().numpy().astype(np.int64)
@@ -772,11 +775,12 @@ def test_pf_matches_oracle(pw, pa, mx, tiled):
 
 @pytest.mark.parametrize("n,k", LLAMA7B)
 @pytest.mark.parametrize("pw,pa", [(2, 8), (4, 4)])
-def test_pf_llama7b_prefill_full(n, k, pw, pa):
+@pytest.mark.parametrize("bn", [128, 192, 256])
+def test_pf_llama7b_prefill_full(n, k, pw, pa, bn):
     """BASELINE configs[2] at full size through APT_KERNEL_PF: EVERY output element vs the oracle."""
     m = 2048
     a = signed_codes(m, k, pa, seed=config_seed(2, pw, pa, salt=13))
     w = signed_codes(n, k, pw, seed=config_seed(2, pw, pa, salt=13) + 1)
     A, W = _pack_both(a, pa, w, pw)
-    got = P.gemm(W, A, config=_pf_cfg(m, n, k, pw, pa)).cpu().numpy().astype(np.int64)
+    got = P.gemm(W, A, config=_pf_cfg(m, n, k, pw, pa, bn=bn)).cpu().numpy().astype(np.int64)
     assert np.array_equal(got, O.gemm_signed_blas(a, w))
