@@ -244,10 +244,13 @@ typedef enum {
                                 16 blocks of 256 K per CTA; > 1 uses the workspace: int32 partials + one
                                 ticket per row tile, see apt_gemm_workspace_bytes).  Needs
                                 Kpad * 255 * 255 < 2^32 (digits are rebuilt as u * 2^s). */
-  APT_KERNEL_PF = 6          /* persistent tcgen05 GEMM for token-rich shapes: one CTA per SM walks the 128 x 128
+  APT_KERNEL_PF = 6          /* persistent tcgen05 GEMM for token-rich shapes: one CTA per SM walks the 128 x bn
                                 tiles, every ring continues across tiles, the TMEM accumulator is double-buffered
-                                so dedicated epilogue warps overlap the next tile's MMAs.  bm = bn = 128, bk 128,
-                                stages 6, split_k 1, cluster_n 1; mma_kind i8 or mxf4 (wbits, abits <= 3).    */
+                                so dedicated epilogue warps overlap the next tile's MMAs.  bm 128, bk 128,
+                                split_k 1, cluster_n 1; bn 128 (stages 6; mma_kind i8 or mxf4 with wbits,
+                                abits <= 3), bn 192 (stages 4, i8) or bn 256 (stages 3, i8: weight digits staged
+                                in shared memory).  i8 needs Kpad * 255 * 255 < 2^31.  The analytic choice for
+                                M > 64.                                                                         */
 } apt_kernel;
 
 /* Kernel configuration (the B200 analogue of the paper's tunable hyperparameters, §5.1).

@@ -37,7 +37,11 @@ constexpr int kPfConvPar = APT_PF_CONV_PAR;
 #define APT_PF256_AS 2  // shared-memory A stages of the 256-token tile
 #endif
 constexpr int kPfEpiWarp0 = 4 + 4 * kPfConvPar;       // first epilogue warp
-constexpr int kPfThreads = 32 * (kPfEpiWarp0 + 4);
+#ifndef APT_PF_EPI_PAR
+#define APT_PF_EPI_PAR 1  // epilogue warps per TMEM sub-partition (each takes 1 / APT_PF_EPI_PAR of the columns)
+#endif
+constexpr int kPfEpiPar = APT_PF_EPI_PAR;
+constexpr int kPfThreads = 32 * (kPfEpiWarp0 + 4 * kPfEpiPar);
 
 // BN = tokens per tile (MMA N): 128; 192 (i8 only) — 2 x 192 accumulator columns + the 4 x 32 A ring fill
 // the 512 TMEM columns; 256 (i8 only) — the two accumulators take all 512 columns, so the converters
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(acc_full(b), 1);
-      mbar_init(acc_empty(b), 4);  // the four epilogue warps
+      mbar_init(acc_empty(b), 4 * kPfEpiPar);  // the epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_w) : "memory");
@@ -283,7 +287,8 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
     }
   } else if (warp >= kPfEpiWarp0) {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - kPfEpiWarp0;  // == warp % 4: this warp's TMEM sub-partition
+    const int ew = (warp - kPfEpiWarp0) & 3;  // == warp % 4: this warp's TMEM sub-partition
+    const int eh = (warp - kPfEpiWarp0) >> 2;  // which 1 / kPfEpiPar of the tile's token columns
     const int r = ew * 32 + lane;
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     pdl_wait();  // token row sums / scales and the output may be touched by the previous kernel
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
       mbar_wait(acc_full(buf), (li >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = eh * (BN / kPfEpiPar); c0 < (eh + 1) * (BN / kPfEpiPar); c0 += 32) {
         uint32_t acc[32];
         tmem_ld32(tmem + lane_off + (uint32_t)(buf * BN + c0), acc);
         if constexpr (MX) {
