@@ -32,7 +32,9 @@ constexpr int kPackMaxRows = 256;  // rows per CTA (shared row-sum / row-max slo
 #define APT_PACK_TILED_ROWS 16  // rows per CTA of a tile-major (weight) pack: one or a few quads per thread
 #endif
 #ifndef APT_PACK_WORD_ROWS
-#define APT_PACK_WORD_ROWS 64  // activation packs up to this many rows take one word per thread
+// activation packs up to this many rows take one word per thread (every activation pack: at M = 2048 the
+// word path is 1.3-1.5x faster than quads, profiles/r2_pack_ab.jsonl)
+#define APT_PACK_WORD_ROWS (1 << 30)
 #endif
 
 // bytewise: signed codes (4 per word) -> offset digits u (4 per word), modulo 2^BITS
@@ -353,7 +355,7 @@ static cudaError_t launch_pack_w(const PackArgs& p, const void* x, float* scale,
   }
 }
 
-// activation packs (a digit view, few rows) take one word per thread; everything else quads
+// activation packs (a digit view) take one word per thread; everything else quads
 template <bool QUANT>
 static cudaError_t launch_pack_t(const PackArgs& p, const void* x, float* scale, int bits, cudaStream_t stream) {
   if (p.digits && p.rows <= APT_PACK_WORD_ROWS) return launch_pack_w<QUANT, 1>(p, x, scale, bits, stream);
