@@ -6,7 +6,7 @@
 // with every ring running continuously across tiles, and the accumulator is double-buffered in TMEM, so
 // the epilogue of tile i (dedicated warps) overlaps the MMAs of tile i + 1.
 //
-// CTA = 32 * (8 + 4 kPfConvPar) threads, tile = 128 weight rows x 128 tokens:
+// CTA = 32 * (8 + 4 kConvPar) threads, tile = 128 weight rows x 128 / 192 / 256 tokens:
 //   warp 0      producer (one thread): weight chunks (256 K elements of the tile's 128 rows, every plane: a
 //               4 KB bulk copy per plane in the tile-major layout, one 3-D TMA box otherwise) into a slot
 //               ring — requested before griddepcontrol.wait for the first tiles, weights never depend on
@@ -14,7 +14,7 @@
 //   warp 1      MMA issuer (one thread): 4 x tcgen05.mma (kind::i8 K=32, or kind::mxf4 K=64) per step into
 //               accumulator buffer (tile & 1); waits until the epilogue released that buffer;
 //   warp 2      TMEM allocation (512 columns: 2 x 128 accumulator, 4 x 32 A ring, 32 mxf4 scale columns);
-//   warps 4..    converters (kPfConvPar per TMEM sub-partition, taking turns by step): planes -> digits
+//   warps 4..    converters (kConvPar per TMEM sub-partition, taking turns by step): planes -> digits
 //               (rebuild8, or rebuild_e2m1 for mxf4) -> tcgen05.st into the A ring;
 //   last 4 warps epilogue (thread = weight row = TMEM lane): tcgen05.ld of the finished buffer, rank-1
 //               corrections and scales (common.cuh arithmetic), stores; then release the buffer.
@@ -29,19 +29,22 @@
 namespace apt {
 
 constexpr int kPfBM = 128;  // weight rows per tile (MMA M)
-#ifndef APT_PF_CONV_PAR
-#define APT_PF_CONV_PAR 2  // converter warps per TMEM sub-partition (steps alternate between them)
-#endif
-constexpr int kPfConvPar = APT_PF_CONV_PAR;
 #ifndef APT_PF256_AS
 #define APT_PF256_AS 2  // shared-memory A stages of the 256-token tile
 #endif
-constexpr int kPfEpiWarp0 = 4 + 4 * kPfConvPar;       // first epilogue warp
 #ifndef APT_PF_EPI_PAR
 #define APT_PF_EPI_PAR 1  // epilogue warps per TMEM sub-partition (each takes 1 / APT_PF_EPI_PAR of the columns)
 #endif
 constexpr int kPfEpiPar = APT_PF_EPI_PAR;
-constexpr int kPfThreads = 32 * (kPfEpiWarp0 + 4 * kPfEpiPar);
+// converter warps per TMEM sub-partition (steps alternate between them): one at wbits <= 4 (fewer warps
+// contending for shared memory and issue slots: 1-5% faster on the 192 / 256-token tiles), two at
+// wbits > 4 (the 8-plane rebuild needs the second warp's latency hiding: W8A8 4096^3 73.5 vs 77.1 us)
+template <int WB>
+struct PfWarps {
+  static constexpr int kConvPar = WB <= 4 ? 1 : 2;
+  static constexpr int kEpiWarp0 = 4 + 4 * kConvPar;  // first epilogue warp
+  static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kPfEpiPar);
+};
 
 // BN = tokens per tile (MMA N): 128; 192 (i8 only) — 2 x 192 accumulator columns + the 4 x 32 A ring fill
 // the 512 TMEM columns; 256 (i8 only) — the two accumulators take all 512 columns, so the converters
@@ -68,7 +71,7 @@ struct PfSmem {
 };
 
 template <int WB, bool MX, int BN>
-__global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_constant__ CUtensorMap tm_w,
+__global__ void __launch_bounds__(PfWarps<WB>::kThreads, 1) gemm_pf_kernel(const __grid_constant__ CUtensorMap tm_w,
                                                                const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
   static_assert(BN == 128 || ((BN == 192 || BN == 256) && !MX), "token tile");
   using L = PfSmem<WB, MX, BN>;
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
         tc_commit(acc_full(buf));
       }
     }
-  } else if (warp >= 4 && warp < kPfEpiWarp0) {
+  } else if (warp >= 4 && warp < PfWarps<WB>::kEpiWarp0) {
     // ------------------------------------------------------------ converters
     const int cw = warp - 4, sub = cw & 3, par = cw >> 2;
     const int r = sub * 32 + lane;
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
     const uint8_t* wsm = gbase + L::kWOff;
     int total = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) total += nsteps;
-    for (int gs = par; gs < total; gs += kPfConvPar) {
+    for (int gs = par; gs < total; gs += PfWarps<WB>::kConvPar) {
       const int gc = MX ? gs : gs >> 1, q = MX ? 0 : gs & 1;
       const int slot = gc % WS;
       mbar_wait(wfull(slot), (gc / WS) & 1);
@@ -285,10 +288,10 @@ __global__ void __launch_bounds__(kPfThreads, 1) gemm_pf_kernel(const __grid_con
         if (lane == 0) mbar_arrive(a_full(a));
       }
     }
-  } else if (warp >= kPfEpiWarp0) {
+  } else if (warp >= PfWarps<WB>::kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
-    const int ew = (warp - kPfEpiWarp0) & 3;  // == warp % 4: this warp's TMEM sub-partition
-    const int eh = (warp - kPfEpiWarp0) >> 2;  // which 1 / kPfEpiPar of the tile's token columns
+    const int ew = (warp - PfWarps<WB>::kEpiWarp0) & 3;  // == warp % 4: this warp's TMEM sub-partition
+    const int eh = (warp - PfWarps<WB>::kEpiWarp0) >> 2;  // which 1 / kPfEpiPar of the tile's token columns
     const int r = ew * 32 + lane;
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     pdl_wait();  // token row sums / scales and the output may be touched by the previous kernel
@@ -402,7 +405,7 @@ static cudaError_t launch_pf2(const CUtensorMap& tw, const CUtensorMap& tb, cons
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = ((p.e.N + kPfBM - 1) / kPfBM) * ((p.e.M + BN - 1) / BN);
   const int grid = tiles < sms ? tiles : sms;
-  return launch_pdl(gemm_pf_kernel<WB, MX, BN>, dim3(grid), dim3(kPfThreads), L::kTotal, stream, dim3(1, 1, 1), tw, tb, p);
+  return launch_pdl(gemm_pf_kernel<WB, MX, BN>, dim3(grid), dim3(PfWarps<WB>::kThreads), L::kTotal, stream, dim3(1, 1, 1), tw, tb, p);
 }
 
 cudaError_t launch_gemm_pf(const TcArgs& p, int wbits, int mx, int bn, cudaStream_t stream) {
