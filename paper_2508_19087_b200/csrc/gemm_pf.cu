@@ -32,18 +32,17 @@ constexpr int kPfBM = 128;  // weight rows per tile (MMA M)
 #ifndef APT_PF256_AS
 #define APT_PF256_AS 2  // shared-memory A stages of the 256-token tile
 #endif
-#ifndef APT_PF_EPI_PAR
-#define APT_PF_EPI_PAR 1  // epilogue warps per TMEM sub-partition (each takes 1 / APT_PF_EPI_PAR of the columns)
-#endif
-constexpr int kPfEpiPar = APT_PF_EPI_PAR;
 // converter warps per TMEM sub-partition (steps alternate between them): one at wbits <= 4 (fewer warps
 // contending for shared memory and issue slots: 1-5% faster on the 192 / 256-token tiles), two at
-// wbits > 4 (the 8-plane rebuild needs the second warp's latency hiding: W8A8 4096^3 73.5 vs 77.1 us)
-template <int WB>
+// wbits > 4 (the 8-plane rebuild needs the second warp's latency hiding: W8A8 4096^3 73.5 vs 77.1 us).
+// EP = epilogue warps per sub-partition (each drains 1 / EP of the tile's token columns): 2 for short
+// walks (<= 8 tiles per CTA, where the last tile's exposed epilogue matters: 3-6% on the prefill shapes),
+// 1 for long ones (the extra warps cost 3% over the 25-tile Llama-3-70B walk)
+template <int WB, int EP>
 struct PfWarps {
   static constexpr int kConvPar = WB <= 4 ? 1 : 2;
   static constexpr int kEpiWarp0 = 4 + 4 * kConvPar;  // first epilogue warp
-  static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * kPfEpiPar);
+  static constexpr int kThreads = 32 * (kEpiWarp0 + 4 * EP);
 };
 
 // BN = tokens per tile (MMA N): 128; 192 (i8 only) — 2 x 192 accumulator columns + the 4 x 32 A ring fill
@@ -70,8 +69,8 @@ struct PfSmem {
   static constexpr int kTotal = kBarOff + kNumBars * 8 + 16 + 1024;  // + TMEM slot + alignment slack
 };
 
-template <int WB, bool MX, int BN>
-__global__ void __launch_bounds__(PfWarps<WB>::kThreads, 1) gemm_pf_kernel(const __grid_constant__ CUtensorMap tm_w,
+template <int WB, bool MX, int BN, int EP>
+__global__ void __launch_bounds__(PfWarps<WB, EP>::kThreads, 1) gemm_pf_kernel(const __grid_constant__ CUtensorMap tm_w,
                                                                const __grid_constant__ CUtensorMap tm_b, TcArgs p) {
   static_assert(BN == 128 || ((BN == 192 || BN == 256) && !MX), "token tile");
   using L = PfSmem<WB, MX, BN>;
@@ -117,7 +116,7 @@ __global__ void __launch_bounds__(PfWarps<WB>::kThreads, 1) gemm_pf_kernel(const
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(acc_full(b), 1);
-      mbar_init(acc_empty(b), 4 * kPfEpiPar);  // the epilogue warps
+      mbar_init(acc_empty(b), 4 * EP);  // the epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_w) : "memory");
@@ -205,7 +204,7 @@ __global__ void __launch_bounds__(PfWarps<WB>::kThreads, 1) gemm_pf_kernel(const
         tc_commit(acc_full(buf));
       }
     }
-  } else if (warp >= 4 && warp < PfWarps<WB>::kEpiWarp0) {
+  } else if (warp >= 4 && warp < PfWarps<WB, EP>::kEpiWarp0) {
     // ------------------------------------------------------------ converters
     const int cw = warp - 4, sub = cw & 3, par = cw >> 2;
     const int r = sub * 32 + lane;
@@ -221,7 +220,7 @@ __global__ void __launch_bounds__(PfWarps<WB>::kThreads, 1) gemm_pf_kernel(const
     const uint8_t* wsm = gbase + L::kWOff;
     int total = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) total += nsteps;
-    for (int gs = par; gs < total; gs += PfWarps<WB>::kConvPar) {
+    for (int gs = par; gs < total; gs += PfWarps<WB, EP>::kConvPar) {
       const int gc = MX ? gs : gs >> 1, q = MX ? 0 : gs & 1;
       const int slot = gc % WS;
       mbar_wait(wfull(slot), (gc / WS) & 1);
@@ -288,10 +287,10 @@ __global__ void __launch_bounds__(PfWarps<WB>::kThreads, 1) gemm_pf_kernel(const
         if (lane == 0) mbar_arrive(a_full(a));
       }
     }
-  } else if (warp >= PfWarps<WB>::kEpiWarp0) {
+  } else if (warp >= PfWarps<WB, EP>::kEpiWarp0) {
     // ------------------------------------------------------------ epilogue
-    const int ew = (warp - PfWarps<WB>::kEpiWarp0) & 3;  // == warp % 4: this warp's TMEM sub-partition
-    const int eh = (warp - PfWarps<WB>::kEpiWarp0) >> 2;  // which 1 / kPfEpiPar of the tile's token columns
+    const int ew = (warp - PfWarps<WB, EP>::kEpiWarp0) & 3;  // == warp % 4: this warp's TMEM sub-partition
+    const int eh = (warp - PfWarps<WB, EP>::kEpiWarp0) >> 2;  // which 1 / EP of the tile's token columns
     const int r = ew * 32 + lane;
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
     pdl_wait();  // token row sums / scales and the output may be touched by the previous kernel
@@ -308,7 +307,7 @@ __global__ void __launch_bounds__(PfWarps<WB>::kThreads, 1) gemm_pf_kernel(const
       mbar_wait(acc_full(buf), (li >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = eh * (BN / kPfEpiPar); c0 < (eh + 1) * (BN / kPfEpiPar); c0 += 32) {
+      for (int c0 = eh * (BN / EP); c0 < (eh + 1) * (BN / EP); c0 += 32) {
         uint32_t acc[32];
         tmem_ld32(tmem + lane_off + (uint32_t)(buf * BN + c0), acc);
         if constexpr (MX) {
@@ -395,17 +394,26 @@ __global__ void __launch_bounds__(PfWarps<WB>::kThreads, 1) gemm_pf_kernel(const
   }
 }
 
-template <int WB, bool MX, int BN>
-static cudaError_t launch_pf2(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, cudaStream_t stream) {
+template <int WB, bool MX, int BN, int EP>
+static cudaError_t launch_pf3(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, int grid, cudaStream_t stream) {
   using L = PfSmem<WB, MX, BN>;
   static_assert(L::kTotal <= 227 * 1024, "shared memory budget");
-  cudaError_t err = set_smem_once<gemm_pf_kernel<WB, MX, BN>>(L::kTotal);
+  cudaError_t err = set_smem_once<gemm_pf_kernel<WB, MX, BN, EP>>(L::kTotal);
   if (err != cudaSuccess) return err;
+  return launch_pdl(gemm_pf_kernel<WB, MX, BN, EP>, dim3(grid), dim3(PfWarps<WB, EP>::kThreads), L::kTotal, stream,
+                    dim3(1, 1, 1), tw, tb, p);
+}
+
+template <int WB, bool MX, int BN>
+static cudaError_t launch_pf2(const CUtensorMap& tw, const CUtensorMap& tb, const TcArgs& p, cudaStream_t stream) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = ((p.e.N + kPfBM - 1) / kPfBM) * ((p.e.M + BN - 1) / BN);
   const int grid = tiles < sms ? tiles : sms;
-  return launch_pdl(gemm_pf_kernel<WB, MX, BN>, dim3(grid), dim3(PfWarps<WB>::kThreads), L::kTotal, stream, dim3(1, 1, 1), tw, tb, p);
+  if constexpr (BN == 256) {
+    if ((tiles + grid - 1) / grid <= 8) return launch_pf3<WB, MX, BN, 2>(tw, tb, p, grid, stream);
+  }
+  return launch_pf3<WB, MX, BN, 1>(tw, tb, p, grid, stream);
 }
 
 cudaError_t launch_gemm_pf(const TcArgs& p, int wbits, int mx, int bn, cudaStream_t stream) {
